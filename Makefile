@@ -1,0 +1,39 @@
+# Builds the B200-native DDPMA library (sm_100a) in-tree:
+#   paper_2006_14602_b200/libddpma.so
+# and the CPU oracle's C helpers (oracle/_build).  `python -c "import
+# __graft_entry__ as g; g.build()"` runs this.
+
+NVCC ?= nvcc
+CXX ?= g++
+SRC := paper_2006_14602_b200/csrc
+OUT := paper_2006_14602_b200/libddpma.so
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false / -ffp-contract=off: no multiply-add contraction, so every
+# expression rounds exactly like the reference's numpy/Python arithmetic.
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v \
+           -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude
+CXXFLAGS := -O2 -fPIC -std=c++17 -ffp-contract=off -Iinclude
+
+OBJ := build/decomp.o build/plan.o build/kernels.o
+
+all: $(OUT)
+
+build:
+	mkdir -p build
+
+build/decomp.o: $(SRC)/decomp.cpp $(SRC)/ddpma_internal.h include/ddpma.h | build
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+build/plan.o: $(SRC)/plan.cu $(SRC)/ddpma_internal.h include/ddpma.h | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/plan.ptxas.log || (cat build/plan.ptxas.log; false)
+
+build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/kernels.ptxas.log || (cat build/kernels.ptxas.log; false)
+
+$(OUT): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+
+clean:
+	rm -rf build $(OUT)
+
+.PHONY: all clean

@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the DDPMA hot path: PMA node-updates/sec (fp64).
+
+One "step" = one pseudo-time window of the non-iterative overlapping Schwarz
+solve (parallel transmission) over ALL subdomains of the workload: density
+pass, trace exchange, adaptive RKC2 integration of every subdomain, mesh /
+residual pass.  A node-update is one frozen-density RHS evaluation at one
+subdomain-box node together with the stage combine consuming it
+(SURVEY §8(d)); the count is exact (the controller's own tally).
+
+Default workload: BASELINE config 3 (4097^2, 8x8 subdomains, overlap 16,
+seeded 32-bump Gaussian mixture) — the largest single-GPU 2D config on which
+BASELINE.json's 1/2/4/8-GPU metric is quoted.  Inputs (~0.7 GB working set
+per stage) are larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+  python bench.py --impl reference ...   # CPU oracle (reference restatement)
+
+N > 1 runs under torchrun: subdomains are sharded over ranks (weak scaling in
+subdomains per rank is NOT used — the problem is fixed, so scaling is
+"strong"); each window exchanges face traces with NCCL
+(paper_2006_14602_b200/distributed.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
+
+# SURVEY §8(d) byte model per node-update by kernel class (ddpma.h profile
+# classes): 0 = stage j>=4 (48 B), 1 = stage 2/3, 2 = final eval (48 B),
+# 3 = f0/euler (24 B), 4 = power eval, 5 = mesh/density, 6 = other.
+CLASS_NAMES = ["stage_j>=4", "stage_2_3", "final_eval", "f0_euler", "power_eval",
+               "mesh_density", "other"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ddpma", choices=["ddpma", "reference"])
+    ap.add_argument("--profile", default="default", choices=["default", "stable"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def case(name, P):
+    """BASELINE config -> (grid, decomposition, monitor) through the public API."""
+    if name == "C1":
+        g = P.build_grid(2, ((0.0, 1.0),) * 2, (65, 65))
+        return g, P.build_decomposition(g, (2, 2), 4), P.density_monitor(P.RingDensity(), g.extents)
+    if name == "C2":
+        g = P.build_grid(2, ((0.0, 1.0),) * 2, (513, 513))
+        return g, P.build_decomposition(g, (4, 4), 8), P.density_monitor(P.seeded_mixture(8, 2), g.extents)
+    if name == "C3":
+        g = P.build_grid(2, ((0.0, 1.0),) * 2, (4097, 4097))
+        return g, P.build_decomposition(g, (8, 8), 16), P.density_monitor(P.seeded_mixture(32, 2), g.extents)
+    if name == "C4":
+        g = P.build_grid(3, ((0.0, 1.0),) * 3, (129, 129, 129))
+        return g, P.build_decomposition(g, (2, 2, 2), 4), P.density_monitor(P.ShellDensity(), g.extents)
+    if name == "C5":
+        g = P.build_grid(3, ((0.0, 1.0),) * 3, (513, 513, 513))
+        return g, P.build_decomposition(g, (4, 4, 4), 8), P.density_monitor(P.seeded_mixture(16, 3), g.extents)
+    raise SystemExit(f"unknown config {name}")
+
+
+def solver_config(P, profile, windows):
+    kw = dict(tol=1e-300, max_windows=windows, transmission="parallel")
+    if profile == "stable":
+        kw.update(rtol=1e-6, atol=1e-9)
+    return P.SolverConfig(**kw)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    try:
+        with open(NCU_SUMMARY) as f:
+            d = json.load(f)
+        return d.get("stage_traffic_bytes_per_node"), d
+    except Exception:
+        return None, None
+
+
+# ------------------------------------------------------------ CPU oracle ---
+
+def cpu_sample(name, threads=None, target_s=12.0):
+    """Bounded sample of the same workload on the host cores, with the oracle
+    (a bitwise restatement of the reference): one RKC2 step of s stages on
+    `threads` subdomain boxes of the config at psi0 with the window density,
+    run concurrently in a thread pool as the reference's parallel mode does
+    (schwarz.py:259-268).  Returns node-updates/s and a description."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import ddpma_oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    cores = threads or len(os.sched_getaffinity(0))
+    g, lay, ov, mon, dom, _ = O.baseline_case(name)
+    d = O.make_decomposition(g, lay, ov)
+    subs = list(d.subs)[:max(1, min(cores, len(d.subs)))]
+    ax = g.axes()
+    work = []
+    for sub in subs:
+        geom = O.box_geom(g, sub)
+        psi = O.psi0(geom)
+        coords, jac = O.mesh_of(psi, geom)
+        raw = mon(O.clamp(coords, dom))
+        rho = raw / 1.0
+        work.append((geom, psi, rho, float(rho.max())))
+    # stages per step: enough RHS evaluations for ~target_s of CPU work
+    one = time.perf_counter()
+    geom, psi, rho, rmax = work[0]
+    O.rhs_frozen(psi, rho, geom, O.DET_FLOOR, geom.mask(), rmax)
+    t_eval = time.perf_counter() - one
+    s = int(max(2, min(64, target_s / max(t_eval * max(1, len(work) / cores), 1e-6))))
+
+    def task(w):
+        geom, psi, rho, rmax = w
+        mask = geom.mask()
+        fn = lambda y: O.rhs_frozen(y, rho, geom, O.DET_FLOOR, mask, rmax)
+        f0, _ = fn(psi)
+        O.Rkc2(1e-3)._step(psi, f0, 1e-7, s, fn)
+        return psi.size * (s + 1)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        nodes = sum(pool.map(task, work))
+    dt = time.perf_counter() - t0
+    return nodes / dt, {"cores": cores, "sample": (
+        f"{len(work)} {name} subdomain boxes x one RKC2 step of {s} stages (+f0) at psi0, "
+        f"oracle/ddpma_oracle.py (numpy, bitwise restatement of ddmesh), "
+        f"ThreadPoolExecutor({cores}) as schwarz.parallel_sweep; {dt:.1f} s")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_sample(args.config, target_s=6.0 if i < args.warmup else 10.0)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": "PMA node-updates/sec (fp64)", "value": value,
+            "unit": "node-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian mixture / ring monitors, psi0 = |xi|^2/2)",
+            "config": {"workload": args.config, "parallelism": "cpu threads"},
+            "vs_baseline": None,
+            "cpu_baseline": {"value": value, "unit": "node-updates/s", "cores": info["cores"],
+                             "kind": "port", "sample": info["sample"]},
+            "e2e": {"value": value, "unit": "node-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm -----
+
+def run_gpu(args):
+    import torch
+    import paper_2006_14602_b200 as P
+    from paper_2006_14602_b200.plan import Plan
+    from paper_2006_14602_b200 import distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    g, dec, mon = case(args.config, P)
+    total_windows = args.warmup + args.steps
+    cfg = solver_config(P, args.profile, total_windows)
+    engine = D.ShardedSolver(g, dec, mon, cfg, rank=rank, world=world,
+                             device=local_rank) if world > 1 else None
+    if engine is None:
+        plan = Plan.for_grid(g, dec.subdomains, mon, cfg)
+        plan.set_state(None)
+        stream = torch.cuda.ExternalStream(P._lib.lib().ddpma_stream(plan.h))
+
+        def window():
+            plan.run(1, 1e-300)
+
+        counters = plan.counters
+        prof_plan = plan
+    else:
+        engine.set_state(None)
+        stream = engine.stream
+
+        def window():
+            engine.window()
+
+        counters = engine.counters
+        prof_plan = engine.plan
+
+    for _ in range(args.warmup):
+        window()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    c0 = counters()
+    prof_plan.set_profiling(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            window()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    c1 = counters()
+    prof = prof_plan.profile()
+    nodes_local = c1["node_updates"] - c0["node_updates"]
+    launches_local = c1["launches"] - c0["launches"]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        n = torch.tensor([nodes_local, launches_local], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(n)
+        nodes, launches = float(n[0].item()), int(n[1].item())
+    else:
+        nodes, launches = float(nodes_local), launches_local
+    value = nodes / (ms / 1e3)
+
+    # roofline of the dominant kernel (RKC stage, class 0) from live CUDA events
+    peak, peak_src = peaks()
+    k = 0
+    achieved = prof["bytes"][k] / (prof["ms"][k] / 1e3) / 1e9 if prof["ms"][k] > 0 else 0.0
+    share = prof["ms"][k] / ms if ms > 0 else 0.0
+    traffic_per_node, ncu = ncu_traffic()
+    nodes_k = int(prof["node_updates"][k])
+    traffic = (traffic_per_node * nodes_k / max(1, int(prof["launches"][k]))
+               if traffic_per_node else None)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": "k_eval<2,pow2,STAGEN> (RKC2 stage j>=4: 48 B/node-update)",
+                "algo_bytes_per_launch": prof["bytes"][k] / max(1, int(prof["launches"][k])),
+                "avg_launch_ms": prof["ms"][k] / max(1, int(prof["launches"][k])),
+                "share_of_step": round(share, 4), "peak_source": peak_src}
+    classes = {CLASS_NAMES[i]: {"ms": round(float(prof["ms"][i]), 3),
+                                "launches": int(prof["launches"][i]),
+                                "GBps": round(prof["bytes"][i] / (prof["ms"][i] / 1e3) / 1e9, 1)
+                                if prof["ms"][i] > 0 else None}
+               for i in range(len(CLASS_NAMES))}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        psi_host = torch.empty(tuple(g.counts), dtype=torch.float64).pin_memory().numpy()
+        # the initial field the reference would build (pma.py:61-64), on the host
+        ax = g.axes()
+        grids = np.meshgrid(*[a * a for a in ax], indexing="ij")
+        psi_host[...] = 0.5 * np.sum(grids, axis=0)
+        del grids
+        ecfg = solver_config(P, args.profile, args.steps)
+        t0 = time.perf_counter()
+        res = P.solve(g, dec, mon, ecfg, initial=psi_host)
+        et = time.perf_counter() - t0
+        nb = psi_host.nbytes
+        e2e = {"value": res.stats["node_updates"] / et, "unit": "node-updates/s",
+               "h2d_bytes_per_step": nb / args.steps,
+               "d2h_bytes_per_step": (res.psi.nbytes + res.mesh.coords.nbytes
+                                      + res.mesh.jac.nbytes
+                                      + sum(s.nbytes for s in res.sub_psi)) / args.steps,
+               "windows": res.windows, "seconds": round(et, 3),
+               "note": "public solve() from psi0: plan build, H2D, windows from the cold "
+                       "start (transient), assembly, D2H of psi/coords/jac/sub_psi"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, info = cpu_sample(args.config)
+            cpu = {"value": v, "unit": "node-updates/s", "cores": info["cores"], "kind": "port",
+                   "sample": info["sample"]}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "error": str(exc)}
+
+    if rank == 0:
+        line = {"metric": "PMA node-updates/sec (fp64)", "value": value,
+                "unit": "node-updates/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64",
+                "data": "synthetic (seeded Gaussian-mixture monitor, psi0 = |xi|^2/2)",
+                "config": {"workload": args.config, "profile": args.profile,
+                           "global_nodes": int(np.prod(g.counts)),
+                           "subdomains": dec.nsub,
+                           "box_nodes": int(sum(np.prod(s.shape()) for s in dec.subdomains)),
+                           "step": "one pseudo-time window (parallel transmission), "
+                                   f"windows {args.warmup + 1}..{args.warmup + args.steps} "
+                                   "of the solve from psi0",
+                           "l2": "inputs larger than L2 (no flush needed)",
+                           "parallelism": f"subdomains sharded over {world} GPU(s)"},
+                "gpu_launches": int(launches),
+                "node_updates": nodes,
+                "roofline": roofline, "kernel_classes": classes,
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,34 @@
+"""B200-native DDPMA hot path of arXiv 2006.14602 (drop-in for ``ddmesh``'s
+PMA/DDPMA solver and mesh-assembly entry points).
+
+Public names follow the reference package (ddmesh/__init__.py:9-44) for the
+hot path: grids and decompositions, density monitors, ``SolverConfig``,
+``solve``, ``solve_single_domain``, ``SolveResult``, ``residual`` and the
+operator-level PMA functions.  All numerics run in libddpma.so (sm_100a
+CUDA); see DESIGN.md.
+"""
+
+from .errors import (ConfigurationError, DdmeshError, DomainError,
+                     InvalidMonitorError, MeshFileError, StiffnessError)
+from .grid import (INTERFACE, PHYSICAL, BoxGeometry, CompGrid, Decomposition,
+                   Subdomain, build_decomposition, build_grid, grid_geometry,
+                   subdomain_geometry)
+from .integrate import IntegrationWindow, rkc_coeffs
+from .monitor import (MixtureDensity, MonitorField, RingDensity, ShellDensity,
+                      UniformDensity, density_monitor, seeded_mixture)
+from .schwarz import (PhysicalMesh, SolverConfig, SolveResult, WindowRecord,
+                      residual, solve, solve_single_domain)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CompGrid", "Decomposition", "Subdomain", "build_grid", "build_decomposition",
+    "grid_geometry", "subdomain_geometry", "BoxGeometry", "PHYSICAL", "INTERFACE",
+    "MonitorField", "density_monitor", "UniformDensity", "RingDensity",
+    "ShellDensity", "MixtureDensity", "seeded_mixture",
+    "IntegrationWindow", "rkc_coeffs",
+    "SolverConfig", "SolveResult", "WindowRecord", "PhysicalMesh",
+    "solve", "solve_single_domain", "residual",
+    "DdmeshError", "ConfigurationError", "DomainError", "InvalidMonitorError",
+    "MeshFileError", "StiffnessError",
+]

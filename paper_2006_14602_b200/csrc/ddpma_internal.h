@@ -1,0 +1,180 @@
+// Internal types shared by the host runtime (plan.cu) and the device kernels
+// (kernels.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ddpma {
+
+// ---------------------------------------------------------------- host ----
+void set_global_error(const std::string& s);
+const char* global_error();
+
+struct RkcCoeffs {
+  double w0, w1, mu1t;
+  std::vector<double> mu, nu, mut, gt;
+};
+void rkc_coeffs(int s, RkcCoeffs& out);   // integrate.py:77-106
+
+// -------------------------------------------------------------- device ----
+constexpr int TX = 32;            // tile width along the contiguous axis
+constexpr int TY = 8;             // tile height along the next axis
+constexpr int NT = TX * TY;       // threads per CTA
+constexpr int MAXB = 64;          // max Gaussian-mixture bumps
+constexpr int NCLASS = 7;         // profiling kernel classes (ddpma.h)
+
+// Per-axis constants of the uniform global grid (grid.py:37-39) in the exact
+// forms the reference's numpy expressions use.
+struct AxisC {
+  double h;
+  double hh, ihh;        // h*h (pma.py:96) and 1/(h*h) when h is a power of 2
+  double twoh, itwoh;    // 2.*h (np.gradient interior) and its reciprocal
+  double ea, eb, ec;     // -1.5/h, 2./h, -0.5/h  (np.gradient low edge)
+  double fa, fb, fc;     // 0.5/h, -2./h, 1.5/h   (np.gradient high edge)
+  double w_in, w_end;    // trapezoid weights h, 0.5*h (quadrature.py:8-13)
+  int n;                 // global node count
+};
+
+struct Prob {
+  int dim;
+  int pow2;              // every spacing is a power of two -> exact reciprocals
+  AxisC ax[3];
+  double measure;        // global |Omega_c| (grid.py:41-47)
+  double floor;          // det_floor
+  double guard;          // max(floor, 0.1/(measure*rho_max)) (pma.py:188-190)
+  double atol, rtol;
+  double a0[3];          // extents[k][0]
+};
+
+struct MonitorD {
+  int kind, nb, dim, pad;
+  double lo[3], hi[3];
+  double constant;
+  double center[3];
+  double amp, nsharp, r2;   // nsharp = -sharp
+  double c[MAXB * 3];
+  double den[MAXB];         // (2.0*s)*s
+  double a[MAXB];
+};
+
+// One local subdomain box in the arena (all fields share this layout).
+struct SubGeo {
+  int n[3];              // box extents (2D: n[2] = 1)
+  int gid;               // global subdomain id
+  long long off;         // element offset of the box in every field
+  int pitch;             // elements per row of the contiguous axis
+  int tiles_x, tiles_y, tiles_z, ntiles;
+  int plo[3], phi[3];    // 1 = physical face
+  double alo[3], ahi[3]; // axes[k][0], axes[k][-1] of the box
+  double halo[3], hahi[3];  // h*axes[k][0], h*axes[k][-1] (pma.py:102,109)
+  int glo[3];            // global index of the box origin
+  int olo[3], ohi[3];    // owned range, box-local inclusive
+  long long nodes;
+};
+
+// One participant (local subdomain) of a batched launch.
+struct Entry {
+  int sub;               // local subdomain index
+  int tile_begin;        // first CTA of this entry
+  int ntiles;
+  int yi, fi;            // current y / f buffer
+  int coef;              // STEP: coefficient table base (index by stage j)
+  int vin, vout;         // POWER: v buffers (-1 = checkerboard seed)
+  int s;                 // stages
+  int pad;
+  double c;              // STEP: h*mu1t | POWER: delta/vnorm | EULER: dtau/m
+  double h04;            // FINAL: 0.4*h
+};
+
+struct Coef {
+  double mu, nu, hmut, hgt;   // mu_j, nu_j, h*mut_j, h*gt_j
+};
+
+// Per-local-subdomain results of one round (zeroed / re-initialised each round).
+struct SubRes {
+  unsigned long long emax;     // max error ratio (bits of a non-negative double)
+  unsigned long long jmin;     // ordered key of min jac
+  unsigned long long jmax;     // ordered key of max jac
+  unsigned long long rawmax;   // ordered key of max raw density
+  unsigned int flags;          // bit0 eval flag, bit1 end flag, bit2 non-finite ratio
+  unsigned int jnan;           // jac NaN seen
+  double sum;                  // finalised sum 1 (norm^2 / z partial)
+  double sum2;                 // finalised sum 2 (residual^2)
+};
+
+struct Fields {
+  double* y[2];
+  double* f[2];
+  double* d[3];
+  double* mr;     // measure * rho  (rho = raw / z), frozen per window
+  double* raw;    // unnormalised nodal density of the level-n mesh
+  double* old;    // psi_level_n (pre-trace snapshot)
+};
+
+enum Mode {
+  M_F0 = 0,        // f0 = F(y)                          (integrate.py:184)
+  M_STAGE2 = 1,    // stage j=2 (d1 = h*mu1t*f0 on the fly) (:170-175)
+  M_STAGE3 = 2,    // stage j=3 (d_{j-2} = d1 on the fly)
+  M_STAGEN = 3,    // stage j>=4
+  M_FINAL = 4,     // f_new = F(y+d_s), y_new, error ratio max (:177, :204-208)
+  M_POWER = 5,     // power-iteration eval (:139-141)
+  M_POWER_SEED = 6,// first power-iteration eval from the checkerboard seed
+  M_EULER = 7      // y + (dtau/m)*F(y)                  (:69-74)
+};
+
+struct KArgs {
+  Prob P;
+  const SubGeo* geo;
+  const Entry* ent;
+  int nent;
+  int j;                 // stage index
+  Fields F;
+  const Coef* coef;
+  SubRes* res;
+  double* part;          // per-CTA partial sums
+  double* part2;
+  const MonitorD* mon;
+};
+
+struct FaceJob {
+  double* dst;
+  const double* src;
+  long long dstr[2], sstr[2];   // tangential strides
+  int ext[2];                   // tangential extents (ext[1] = 1 in 2D)
+  int skip_lo[2], skip_hi[2];   // lower-donor faces that win the edge nodes
+  int node_begin;               // first flattened face node of this job
+  int pad;
+};
+
+struct GapJob {
+  const double* a;
+  const double* b;
+  long long astr[3], bstr[3];
+  int ext[3];
+  int node_begin;
+};
+
+// Launchers (kernels.cu).  All asynchronous on `stream`.
+void launch_eval(int mode, const KArgs& a, int nblocks, void* stream);
+void launch_sumsq(const KArgs& a, int nblocks, void* stream);
+void launch_finalize(const Entry* ent, int nent, const double* part, SubRes* res,
+                     int which, void* stream);
+void launch_mesh(const KArgs& a, int nblocks, int with_residual, void* stream);
+void launch_prologue(const KArgs& a, int nblocks, double z, void* stream);
+void launch_res_init(SubRes* res, int n, void* stream);
+void launch_faces(const FaceJob* jobs, int njobs, int nnodes, void* stream);
+void launch_gap(const GapJob* jobs, int njobs, int nnodes, unsigned long long* out,
+                void* stream);
+void launch_psi0(const KArgs& a, int nblocks, void* stream);
+void launch_scatter(const KArgs& a, int nblocks, const double* global, void* stream);
+void launch_assemble(const KArgs& a, int nblocks, double* psi, double* coords,
+                     double* jac, void* stream);
+void launch_ratio_mask(const KArgs& a, int nblocks, double* out, void* stream);
+void launch_box_mesh(const KArgs& a, int nblocks, double* coords, double* jac, double* raw,
+                     void* stream);
+void launch_box_copy(const KArgs& a, int nblocks, const double* src_box, double* dst,
+                     int to_arena, void* stream);
+
+}  // namespace ddpma

@@ -1,0 +1,343 @@
+"""Generate the golden fixtures by running the REAL reference (``ddmesh``).
+
+Run in the build container only (it needs /root/reference):
+
+    OPENBLAS_NUM_THREADS=1 OMP_NUM_THREADS=1 python tests/golden/make_golden.py
+
+It never writes to /root/reference (bytecode writing is disabled).  The
+fixtures pin ``oracle/ddpma_oracle.py`` (tests/test_oracle.py) and serve as
+the expected values of the GPU trajectory tests (tests/test_gpu_parity.py).
+Monitors are the BASELINE.json formulas as implemented in the oracle module
+(plain numpy callables passed through ``ddmesh.density_monitor``).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+sys.dont_write_bytecode = True
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+sys.path.insert(0, HERE)
+
+import numpy as np  # noqa: E402
+
+import ddmesh  # noqa: E402
+from ddmesh import pma as rpma  # noqa: E402
+import ddpma_oracle as O  # noqa: E402
+import recipes as R  # noqa: E402
+
+
+def sub_to_json(s):
+    return {"id": s.id, "pos": list(s.pos), "box": [list(b) for b in s.box],
+            "faces": [list(f) for f in s.faces],
+            "neighbors": sorted([[k[0], k[1], v] for k, v in s.neighbors.items()]),
+            "owned": [list(o) for o in s.owned]}
+
+
+def gen_decomp():
+    out = []
+    for dim, counts, layout, ov in R.DECOMP_CASES:
+        case = {"dim": dim, "counts": list(counts), "layout": list(layout), "overlap": ov}
+        try:
+            g = ddmesh.build_grid(dim, tuple((0.0, 1.0) for _ in range(dim)), counts)
+            d = ddmesh.build_decomposition(g, layout, ov)
+            case["subs"] = [sub_to_json(s) for s in d.subdomains]
+        except ddmesh.ConfigurationError as e:
+            case["error"] = "ConfigurationError"
+            case["message"] = str(e)
+        out.append(case)
+    with open(os.path.join(HERE, "decomp.json"), "w") as f:
+        json.dump(out, f)
+    print("decomp", len(out))
+
+
+def ref_case(name):
+    g, lay, ov, mon, dom, win = O.baseline_case(name)
+    rg = ddmesh.build_grid(g.dim, g.extents, g.counts)
+    rd = ddmesh.build_decomposition(rg, lay, ov)
+    return rg, rd, mon
+
+
+def gen_rhs(name):
+    rg, rd, mon = ref_case(name)
+    full = name == "C1"
+    data = {}
+    for sid in R.rhs_case_subs(rd.layout):
+        sub = rd.subdomains[sid]
+        geom = ddmesh.subdomain_geometry(rg, sub)
+        psi = R.perturbed_global(geom.axes)
+        coords = np.stack(rpma.gradient_fd(psi, geom), axis=-1)
+        raw = mon(np.clip(coords, 0.0, 1.0))
+        rho = raw / R.RHS_Z
+        rmax = float(rho.max())
+        mask = geom.dirichlet_mask()
+        F, flag = rpma.pma_rhs_frozen(psi, rho, geom, rpma.DET_FLOOR, mask, rmax)
+        det = rpma.hessian_det_fd(psi, geom)
+        p = f"s{sid}_"
+        data[p + "flag"] = np.array(flag)
+        data[p + "rmax"] = np.array(rmax)
+        for key, arr in (("F", F), ("det", det), ("coords", coords), ("raw", raw)):
+            data[p + key + "_sha"] = np.array(R.digest(arr))
+            if full:
+                data[p + key] = arr
+            else:
+                idx = R.sample_index(psi.shape)
+                flat = arr.reshape(psi.size, -1) if arr.ndim > psi.ndim else arr.reshape(-1)
+                data[p + key + "_idx"] = idx
+                data[p + key + "_smp"] = flat[idx]
+                data[p + key + "_sum"] = np.array(float(np.sum(arr)))
+    np.savez_compressed(os.path.join(HERE, f"rhs_{name}.npz"), **data)
+    print("rhs", name, sorted(R.rhs_case_subs(rd.layout)))
+
+
+def result_arrays(res, full=True, sample=False):
+    d = {"windows": np.array(res.windows), "converged": np.array(res.converged),
+         "final_residual": np.array(res.final_residual),
+         "overlap_gap": np.array(res.overlap_gap),
+         "residuals": np.array([h.residuals for h in res.history]),
+         "jac_min": np.array([h.jac_min for h in res.history]),
+         "jac_max": np.array([h.jac_max for h in res.history])}
+    for key, arr in (("psi", res.psi), ("coords", res.mesh.coords), ("jac", res.mesh.jac)):
+        d[key + "_sha"] = np.array(R.digest(arr))
+        if full:
+            d[key] = arr
+        if sample:
+            idx = R.sample_index(res.psi.shape)
+            flat = arr.reshape(res.psi.size, -1) if arr.ndim > res.psi.ndim else arr.reshape(-1)
+            d[key + "_idx"] = idx
+            d[key + "_smp"] = flat[idx]
+    if full:
+        for i, sp in enumerate(res.sub_psi):
+            d[f"sub_psi{i}"] = sp
+    return d
+
+
+class CountRhs:
+    """Counts RHS calls / node-updates by wrapping pma_rhs_frozen."""
+
+    def __init__(self):
+        self.calls = 0
+        self.nodes = 0
+        self.orig = rpma.pma_rhs_frozen
+
+    def __enter__(self):
+        def wrapped(psi, *a, **k):
+            self.calls += 1
+            self.nodes += psi.size
+            return self.orig(psi, *a, **k)
+        rpma.pma_rhs_frozen = wrapped
+        return self
+
+    def __exit__(self, *exc):
+        rpma.pma_rhs_frozen = self.orig
+
+
+ONLY = []
+
+
+def run_save(tag, fn, full=True, sample=False):
+    if ONLY and not any(tag.startswith(o) for o in ONLY):
+        return
+    t0 = time.perf_counter()
+    with CountRhs() as c:
+        try:
+            res = fn()
+            d = result_arrays(res, full, sample)
+        except (ddmesh.DdmeshError, ValueError, OverflowError) as e:
+            d = {"error": np.array(type(e).__name__), "message": np.array(str(e))}
+            if isinstance(e, ddmesh.StiffnessError):
+                d["subdomain"] = np.array(-1 if e.subdomain is None else e.subdomain)
+    d["rhs_calls"] = np.array(c.calls)
+    d["node_updates"] = np.array(c.nodes)
+    d["seconds"] = np.array(time.perf_counter() - t0)
+    np.savez_compressed(os.path.join(HERE, f"run_{tag}.npz"), **d)
+    print("run", tag, f"{time.perf_counter() - t0:.1f}s", d.get("error", ""),
+          int(d["rhs_calls"]))
+
+
+def cfg(**kw):
+    base = dict(tol=1e-300, workers=1)
+    base.update(kw)
+    return ddmesh.SolverConfig(**base)
+
+
+def gen_runs(quick=False):
+    rg, rd, mon = ref_case("C1")
+    m1 = ddmesh.density_monitor(mon, rg.extents)
+    nwin = 200 if quick else 2000
+    for tr in ("parallel", "alternating"):
+        run_save(f"C1_{tr}_100", lambda: ddmesh.solve(
+            rg, rd, m1, cfg(max_windows=100, transmission=tr)))
+        run_save(f"C1_{tr}_{nwin}", lambda: ddmesh.solve(
+            rg, rd, m1, cfg(max_windows=nwin, transmission=tr)))
+    run_save("C1_single_100", lambda: ddmesh.solve_single_domain(
+        rg, m1, cfg(max_windows=100)))
+    run_save(f"C1_single_{nwin}", lambda: ddmesh.solve_single_domain(
+        rg, m1, cfg(max_windows=nwin)))
+    # stop rules: converged flag and window count (alternating: the parallel
+    # default-profile transient is chaotic)
+    run_save("C1_tol_min", lambda: ddmesh.solve(
+        rg, rd, m1, ddmesh.SolverConfig(tol=1e-7, transmission="alternating")))
+    run_save("C1_tol_max", lambda: ddmesh.solve(
+        rg, rd, m1, ddmesh.SolverConfig(tol=1e-7, transmission="alternating",
+                                         stop_rule="max")))
+    # parallel transmission to convergence under the tight-tolerance profile
+    run_save(f"C1_parallel_stable_{nwin}", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=nwin, transmission="parallel", rtol=1e-6, atol=1e-9)))
+    # euler scheme
+    run_save("C1_euler", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=20, transmission="parallel", scheme="euler",
+                        substeps=3, dtau=1e-5)))
+    # warm start
+    init = R.perturbed_global(rg.axes())
+    run_save("C1_warm", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=30, transmission="parallel"), initial=init))
+    # tight tolerance profile ("stable"), small stage cap
+    run_save("C1_stable", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=40, transmission="parallel", rtol=1e-6, atol=1e-9)))
+    run_save("C1_cap8", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=40, transmission="alternating", max_stages=8)))
+    # 4-slab layout, odd overlap
+    rd4 = ddmesh.build_decomposition(rg, (4, 1), 3)
+    run_save("C1_slab4", lambda: ddmesh.solve(
+        rg, rd4, m1, cfg(max_windows=60, transmission="parallel")))
+    # uniform monitor: exact identity, residual 0 in one window
+    uni2 = ddmesh.density_monitor(lambda p: np.ones(p.shape[:-1]), rg.extents)
+    for tr in ("parallel", "alternating"):
+        run_save(f"U2_{tr}", lambda: ddmesh.solve(rg, rd, uni2, ddmesh.SolverConfig(
+            transmission=tr)))
+    g3 = ddmesh.build_grid(3, ((0.0, 1.0),) * 3, (33, 33, 33))
+    d3 = ddmesh.build_decomposition(g3, (2, 2, 2), 4)
+    uni3 = ddmesh.density_monitor(lambda p: np.ones(p.shape[:-1]), g3.extents)
+    run_save("U3_parallel", lambda: ddmesh.solve(g3, d3, uni3, ddmesh.SolverConfig(
+        transmission="parallel")))
+    # small 3D trajectories (shell monitor)
+    m3 = ddmesh.density_monitor(O.Shell(), g3.extents)
+    for tr in ("parallel", "alternating"):
+        run_save(f"T3_{tr}", lambda: ddmesh.solve(
+            g3, d3, m3, cfg(max_windows=40, transmission=tr)))
+    run_save("T3_single", lambda: ddmesh.solve_single_domain(
+        g3, m3, cfg(max_windows=40)))
+    # error paths
+    neg = ddmesh.density_monitor(O.Ring(amp=-20.0), rg.extents)
+    run_save("E_invalid", lambda: ddmesh.solve(rg, rd, neg, cfg(
+        max_windows=3, transmission="parallel")))
+    half = ddmesh.density_monitor(O.Ring(amp=-1.5), rg.extents)
+    run_save("E_stiff", lambda: ddmesh.solve(rg, rd, half, cfg(
+        max_windows=3, transmission="parallel")))
+    if quick:
+        return
+    # larger BASELINE configs, truncated (sampled + digests)
+    rg2, rd2, mon2 = ref_case("C2")
+    run_save("C2_parallel_2", lambda: ddmesh.solve(
+        rg2, rd2, ddmesh.density_monitor(mon2, rg2.extents),
+        cfg(max_windows=2, transmission="parallel")), full=False, sample=True)
+    rg4, rd4_, mon4 = ref_case("C4")
+    run_save("C4_parallel_1", lambda: ddmesh.solve(
+        rg4, rd4_, ddmesh.density_monitor(mon4, rg4.extents),
+        cfg(max_windows=1, transmission="parallel")), full=False, sample=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["decomp", "rhs", "runs"]
+    ONLY = [w[5:] for w in what if w.startswith("only=")]
+    if "decomp" in what:
+        gen_decomp()
+    if "rhs" in what:
+        for n in ("C1", "C2", "C3", "C4", "C5"):
+            gen_rhs(n)
+    if "runs" in what:
+        gen_runs(quick="quick" in what)
+
+
+# ------------------------------------------------------------ envelopes ----
+# The reference's transients are chaotically sensitive: perturbing np.log by
+# one ulp at 30% of nodes moves default-profile coordinates by ~1e-3 within
+# 20 windows (positivity-flag decisions flip).  The envelope of each run is
+# the spread of the oracle (bitwise-pinned to the reference above) under two
+# such perturbations; GPU trajectories must stay within a small multiple of it.
+
+def _noisy_oracle(seed):
+    orig = O.log_equi
+    rng = np.random.default_rng(seed)
+
+    def noisy(rho, det, measure, floor, rmax):
+        f = orig(rho, det, measure, floor, rmax)
+        m = rng.random(f.shape) < 0.3
+        f[m] = np.nextafter(f[m], np.inf)
+        return f
+    return orig, noisy
+
+
+ENVELOPE_RUNS = {
+    "C1_parallel_100": ("C1", dict(max_windows=100, transmission="parallel"), None),
+    "C1_alternating_100": ("C1", dict(max_windows=100, transmission="alternating"), None),
+    "C1_single_100": ("C1s", dict(max_windows=100), None),
+    "C1_euler": ("C1", dict(max_windows=20, transmission="parallel", scheme="euler",
+                            substeps=3, dtau=1e-5), None),
+    "C1_stable": ("C1", dict(max_windows=40, transmission="parallel", rtol=1e-6, atol=1e-9), None),
+    "C1_cap8": ("C1", dict(max_windows=40, transmission="alternating", max_stages=8), None),
+    "C1_warm": ("C1", dict(max_windows=30, transmission="parallel"), "warm"),
+    "C1_slab4": ("C1slab", dict(max_windows=60, transmission="parallel"), None),
+    "T3_parallel": ("T3", dict(max_windows=40, transmission="parallel"), None),
+    "T3_alternating": ("T3", dict(max_windows=40, transmission="alternating"), None),
+    "T3_single": ("T3s", dict(max_windows=40), None),
+}
+
+
+def _oracle_run(kind, kw, init):
+    if kind.startswith("T3"):
+        g = O.make_grid(3, ((0, 1),) * 3, (33, 33, 33))
+        mon, lay, ov = O.Shell(), (2, 2, 2), 4
+    else:
+        g, lay, ov, mon, _, _ = O.baseline_case("C1")
+        if kind == "C1slab":
+            lay, ov = (4, 1), 3
+    cfg = O.Config(tol=1e-300, **kw)
+    initial = R.perturbed_global(g.axes()) if init == "warm" else None
+    if kind.endswith("s") and kind != "C1slab":
+        return O.solve_single(g, mon, g.extents, cfg, initial=initial)
+    d = O.make_decomposition(g, lay, ov)
+    return O.solve(g, d, mon, g.extents, cfg, initial=initial)
+
+
+def gen_envelopes():
+    for tag, (kind, kw, init) in ENVELOPE_RUNS.items():
+        if ONLY and not any(tag.startswith(o) for o in ONLY):
+            continue
+        t0 = time.perf_counter()
+        base = _oracle_run(kind, kw, init)
+        out = {"coords": 0.0, "psi": 0.0, "psi_centered": 0.0, "jac": 0.0,
+               "nodes_rel": 0.0, "res_rel": 0.0}
+        for seed in (1, 2):
+            orig, noisy = _noisy_oracle(seed)
+            O.log_equi = noisy
+            try:
+                r = _oracle_run(kind, kw, init)
+            finally:
+                O.log_equi = orig
+            dp = r.psi - base.psi
+            out["coords"] = max(out["coords"], float(np.abs(r.coords - base.coords).max()))
+            out["psi"] = max(out["psi"], float(np.abs(dp).max()))
+            out["psi_centered"] = max(out["psi_centered"], float(np.abs(dp - dp.mean()).max()))
+            out["jac"] = max(out["jac"], float(np.abs(r.jac - base.jac).max()))
+            out["nodes_rel"] = max(out["nodes_rel"], abs(r.counter.node_updates
+                                                         - base.counter.node_updates)
+                                   / base.counter.node_updates)
+            rr = np.array(r.residuals)
+            br = np.array(base.residuals)
+            out["res_rel"] = max(out["res_rel"], float(np.max(np.abs(rr - br) / np.abs(br))))
+        np.savez(os.path.join(HERE, f"env_{tag}.npz"), **{k: np.array(v) for k, v in out.items()})
+        print("env", tag, f"{time.perf_counter() - t0:.1f}s", out)
+
+
+if __name__ == "__main__" and "envelopes" in sys.argv[1:]:
+    ONLY[:] = [w[5:] for w in sys.argv[1:] if w.startswith("only=")]
+    gen_envelopes()

@@ -1,0 +1,312 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden fixtures.  Run on a B200 with ``pytest -m gpu``.
+
+Tolerances (north_star): node coordinates within max-abs 1e-10 relative to
+the domain size at a fixed window count; index ranges and node ordering
+bit-exact.  Pure-arithmetic operator outputs (Hessian determinant, mesh
+coordinates) must be bitwise identical; values through log/exp agree to a
+few ulp (CUDA's fp64 log/exp vs numpy's differ by <= 1 ulp).
+"""
+
+import numpy as np
+import pytest
+
+import ddpma_oracle as O
+import recipes as R
+from conftest import golden
+
+import paper_2006_14602_b200 as P
+from paper_2006_14602_b200 import pma as G
+from paper_2006_14602_b200.plan import Plan
+
+pytestmark = pytest.mark.gpu
+
+COORD_TOL = 1e-10          # max-abs, domain size 1 (north_star)
+
+
+def rel_close(a, b, rtol):
+    a, b = np.asarray(a), np.asarray(b)
+    scale = np.maximum(np.abs(b), 1.0)
+    return float(np.max(np.where(a == b, 0.0, np.abs(a - b) / scale))) <= rtol
+
+
+def ring_case():
+    g = P.build_grid(2, ((0.0, 1.0), (0.0, 1.0)), (65, 65))
+    d = P.build_decomposition(g, (2, 2), 4)
+    m = P.density_monitor(P.RingDensity(), g.extents)
+    return g, d, m
+
+
+def baseline(name):
+    og, lay, ov, omon, dom, win = O.baseline_case(name)
+    g = P.build_grid(og.dim, og.extents, og.counts)
+    d = P.build_decomposition(g, lay, ov)
+    if isinstance(omon, O.Mixture):
+        raw = P.MixtureDensity(omon.c, omon.s, omon.a)
+    else:
+        raw = P.RingDensity(omon.center, omon.amp, omon.sharp, omon.r2)
+    return og, g, d, P.density_monitor(raw, g.extents), lay, raw
+
+
+# ------------------------------------------------------------ operators ----
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_rhs_operator_parity(name):
+    og, g, d, mon, lay, raw = baseline(name)
+    for sid in R.rhs_case_subs(lay):
+        sub = d.subdomains[sid]
+        geom = P.subdomain_geometry(g, sub)
+        ogeom = O.box_geom(og, O.make_decomposition(og, lay, d.overlap).subs[sid])
+        psi = R.perturbed_global(geom.axes)
+        # oracle
+        ocoords = np.stack(O.coords_fd(psi, ogeom), axis=-1)
+        oraw = raw(np.clip(ocoords, 0.0, 1.0))
+        rho = oraw / R.RHS_Z
+        rmax = float(rho.max())
+        oF, oflag = O.rhs_frozen(psi, rho, ogeom, O.DET_FLOOR, ogeom.mask(), rmax)
+        odet = O.hess_det(psi, ogeom)
+        # device
+        mesh = G.physical_mesh(psi, geom)
+        assert np.array_equal(mesh.jac, odet), (name, sid, "det bitwise")
+        assert np.array_equal(mesh.coords, ocoords), (name, sid, "coords bitwise")
+        draw = G.mesh_density(mon, psi, geom)
+        assert rel_close(draw, oraw, 4e-16 * 8), (name, sid, "raw")
+        F, flag = G.pma_rhs_frozen(psi, rho, geom, max_rho=rmax)
+        assert flag == oflag
+        assert rel_close(F, oF, 1e-14), (name, sid, "F")
+        # golden pin of the same case
+        gold = golden(f"rhs_{name}.npz")
+        assert R.digest(mesh.jac) == str(gold[f"s{sid}_det_sha"])
+
+
+def test_rkc_step_parity():
+    g, d, mon = ring_case()
+    og = O.make_grid(2, ((0, 1), (0, 1)), (65, 65))
+    od = O.make_decomposition(og, (2, 2), 4)
+    for sid in (0, 3):
+        geom = P.subdomain_geometry(g, d.subdomains[sid])
+        ogeom = O.box_geom(og, od.subs[sid])
+        y = R.perturbed_global(geom.axes)
+        coords = np.stack(O.coords_fd(y, ogeom), axis=-1)
+        rho = O.Ring()(np.clip(coords, 0, 1)) / 1.3
+        rmax = float(rho.max())
+        fn = lambda v: O.rhs_frozen(v, rho, ogeom, O.DET_FLOOR, ogeom.mask(), rmax)
+        f0, _ = fn(y)
+        integ = O.Rkc2(1e-3)
+        for h, s in ((1e-5, 2), (3e-5, 3), (2e-4, 9), (5e-4, 17)):
+            od_, ofn, ofl, oend = integ._step(y, f0, h, s, fn)
+            with Plan.for_geometry(geom, P.SolverConfig()) as p:
+                dd, fnew, fl, end = p.rkc_step(0, y, rho, rmax, h, s)
+            assert (fl, end) == (ofl, oend)
+            assert rel_close(dd, od_, 1e-12), (sid, h, s)
+            assert rel_close(fnew, ofn, 1e-12), (sid, h, s)
+
+
+def test_rkc_coeffs_bitwise():
+    for s in (2, 3, 7, 23, 100, 512):
+        got = P.rkc_coeffs(s)
+        ref = O.rkc_coeffs(s)
+        for a, b in zip(got, ref):
+            assert np.array_equal(np.asarray(a), np.asarray(b)), s
+
+
+def test_residual_operator():
+    g, d, _ = ring_case()
+    geom = P.subdomain_geometry(g, d.subdomains[1])
+    a = R.perturbed_global(geom.axes)
+    b = R.perturbed_global(geom.axes, eps=0.3)
+    assert rel_close(P.residual(a, b, geom), O.l2_norm(a - b, geom.spacing), 1e-13)
+
+
+# ---------------------------------------------------------- trajectories ---
+
+def envelope(tag):
+    """Spread of the reference itself under 1-ulp log noise (tests/golden/env_*,
+    make_golden.py gen_envelopes) — None for converged runs."""
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, f"env_{tag}.npz")
+    return golden(f"env_{tag}.npz") if os.path.exists(path) else None
+
+
+def check_run(res, gold, tag=None, coord_tol=COORD_TOL):
+    """Trajectory parity at a fixed window count.
+
+    Converged runs (no envelope): coordinates within 1e-10 of the reference
+    (north_star), psi within 1e-10 up to its free additive constant.
+    Transient runs: the reference is chaotically sensitive to 1-ulp changes
+    of np.log (positivity-flag decisions flip), so the
+    device must stay within a small multiple of the reference's own spread
+    under such perturbations — and within 1e-10 wherever that spread is
+    below it (3D shell, Euler)."""
+    env = envelope(tag) if tag else None
+    assert res.windows == int(gold["windows"])
+    assert res.converged == bool(gold["converged"])
+    n_ref = int(gold["node_updates"])
+    n_rel = abs(res.stats["node_updates"] - n_ref) / n_ref
+    n_tol = 0.0 if env is None else 4.0 * float(env["nodes_rel"])
+    if env is None or float(env["nodes_rel"]) == 0.0:
+        n_tol = 0.0 if env is not None else 0.05
+    assert n_rel <= n_tol + 1e-12, (res.stats["node_updates"], n_ref, n_tol)
+    c_tol = coord_tol if env is None else max(coord_tol, 20.0 * float(env["coords"]))
+    p_tol = coord_tol if env is None else max(coord_tol, 20.0 * float(env["psi_centered"]))
+    if "coords" in gold:
+        dc = np.max(np.abs(res.mesh.coords - gold["coords"]))
+        dp = res.psi - gold["psi"]
+        dpc = np.max(np.abs(dp - dp.mean()))
+    else:
+        idx = gold["coords_idx"]
+        flat = res.mesh.coords.reshape(res.psi.size, -1)[idx]
+        dc = np.max(np.abs(flat - gold["coords_smp"]))
+        dp = res.psi.reshape(-1)[gold["psi_idx"]] - gold["psi_smp"]
+        dpc = np.max(np.abs(dp - dp.mean()))
+    print(f"[parity] {tag}: max|dcoords|={dc:.3g} (tol {c_tol:.3g}) "
+          f"max|dpsi-const|={dpc:.3g} nodes_rel={n_rel:.3g}")
+    assert dc <= c_tol, (dc, c_tol)
+    assert dpc <= p_tol, (dpc, p_tol)
+    hr = np.array([h.residuals for h in res.history])
+    assert hr.shape == gold["residuals"].shape
+    r_tol = 1e-6 if env is None else max(1e-6, 20.0 * float(env["res_rel"]))
+    # the last window's residual is the stop quantity
+    assert rel_close(hr[-1], gold["residuals"][-1], r_tol)
+
+
+@pytest.mark.parametrize("tr,nwin", [("parallel", 100), ("alternating", 100),
+                                     ("parallel", 2000), ("alternating", 2000)])
+def test_c1_trajectory(tr, nwin):
+    g, d, m = ring_case()
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=nwin, transmission=tr))
+    tag = f"C1_{tr}_{nwin}"
+    gold = golden(f"run_{tag}.npz")
+    check_run(res, gold, tag)
+    env = envelope(tag)
+    tol = COORD_TOL if env is None else 20.0 * float(env["psi"])
+    for i, sp in enumerate(res.sub_psi):
+        d = sp - gold[f"sub_psi{i}"]
+        assert np.max(np.abs(d - d.mean())) <= tol
+    if env is None:
+        assert abs(res.overlap_gap - float(gold["overlap_gap"])) <= 1e-9
+
+
+@pytest.mark.parametrize("nwin", [100, 2000])
+def test_c1_single_domain(nwin):
+    g, _, m = ring_case()
+    res = P.solve_single_domain(g, m, P.SolverConfig(tol=1e-300, max_windows=nwin))
+    check_run(res, golden(f"run_C1_single_{nwin}.npz"), f"C1_single_{nwin}")
+
+
+def test_one_by_one_equals_single_domain_bitwise():
+    g, _, m = ring_case()
+    cfg = P.SolverConfig(tol=1e-300, max_windows=50)
+    a = P.solve_single_domain(g, m, cfg)
+    b = P.solve(g, P.build_decomposition(g, (1, 1), 3), m, cfg)
+    assert np.array_equal(a.psi, b.psi) and np.array_equal(a.mesh.coords, b.mesh.coords)
+
+
+def test_deterministic_rerun_bitwise():
+    g, d, m = ring_case()
+    cfg = P.SolverConfig(tol=1e-300, max_windows=30, transmission="parallel")
+    a = P.solve(g, d, m, cfg)
+    b = P.solve(g, d, m, cfg)
+    assert np.array_equal(a.psi, b.psi) and np.array_equal(a.mesh.jac, b.mesh.jac)
+
+
+@pytest.mark.parametrize("tag,kw,init", [
+    ("C1_euler", dict(max_windows=20, transmission="parallel", scheme="euler", substeps=3,
+                      dtau=1e-5), False),
+    ("C1_stable", dict(max_windows=40, transmission="parallel", rtol=1e-6, atol=1e-9), False),
+    ("C1_cap8", dict(max_windows=40, transmission="alternating", max_stages=8), False),
+    ("C1_warm", dict(max_windows=30, transmission="parallel"), True),
+])
+def test_c1_variants(tag, kw, init):
+    g, d, m = ring_case()
+    initial = R.perturbed_global(g.axes()) if init else None
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, **kw), initial=initial)
+    check_run(res, golden(f"run_{tag}.npz"), tag)
+
+
+def test_c1_slab4():
+    g, _, m = ring_case()
+    d = P.build_decomposition(g, (4, 1), 3)
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=60, transmission="parallel"))
+    check_run(res, golden("run_C1_slab4.npz"), "C1_slab4")
+
+
+@pytest.mark.parametrize("rule", ["min", "max"])
+def test_c1_stop_rule(rule):
+    g, d, m = ring_case()
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-7, transmission="parallel", stop_rule=rule))
+    gold = golden(f"run_C1_tol_{rule}.npz")
+    assert res.converged
+    # the crossing window of tol=1e-7 may move by a window under ulp noise
+    assert abs(res.windows - int(gold["windows"])) <= 2
+    assert res.final_residual <= 1e-7
+
+
+@pytest.mark.parametrize("tr", ["parallel", "alternating"])
+def test_uniform_monitor_exact(tr):
+    g, d, _ = ring_case()
+    m = P.density_monitor(P.UniformDensity(1.0), g.extents)
+    res = P.solve(g, d, m, P.SolverConfig(transmission=tr))
+    gold = golden(f"run_U2_{tr}.npz")
+    assert res.windows == 1 and res.final_residual == 0.0 and res.converged
+    assert np.array_equal(res.psi, gold["psi"])
+    assert np.array_equal(res.mesh.coords, gold["coords"])
+
+
+def test_uniform_monitor_exact_3d():
+    g = P.build_grid(3, ((0.0, 1.0),) * 3, (33, 33, 33))
+    d = P.build_decomposition(g, (2, 2, 2), 4)
+    m = P.density_monitor(P.UniformDensity(1.0), g.extents)
+    res = P.solve(g, d, m, P.SolverConfig(transmission="parallel"))
+    gold = golden("run_U3_parallel.npz")
+    assert res.windows == 1 and res.final_residual == 0.0
+    assert np.array_equal(res.mesh.coords, gold["coords"])
+
+
+@pytest.mark.parametrize("tr", ["parallel", "alternating"])
+def test_t3_3d_trajectory(tr):
+    g = P.build_grid(3, ((0.0, 1.0),) * 3, (33, 33, 33))
+    d = P.build_decomposition(g, (2, 2, 2), 4)
+    m = P.density_monitor(P.ShellDensity(), g.extents)
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=40, transmission=tr))
+    check_run(res, golden(f"run_T3_{tr}.npz"), f"T3_{tr}")
+
+
+def test_t3_single():
+    g = P.build_grid(3, ((0.0, 1.0),) * 3, (33, 33, 33))
+    m = P.density_monitor(P.ShellDensity(), g.extents)
+    res = P.solve_single_domain(g, m, P.SolverConfig(tol=1e-300, max_windows=40))
+    check_run(res, golden("run_T3_single.npz"), "T3_single")
+
+
+def test_error_paths():
+    g, d, _ = ring_case()
+    neg = P.density_monitor(P.RingDensity(amp=-20.0), g.extents)
+    with pytest.raises(P.InvalidMonitorError):
+        P.solve(g, d, neg, P.SolverConfig(tol=1e-300, max_windows=3, transmission="parallel"))
+    half = P.density_monitor(P.RingDensity(amp=-1.5), g.extents)
+    with pytest.raises(ValueError) as ei:
+        P.solve(g, d, half, P.SolverConfig(tol=1e-300, max_windows=3, transmission="parallel"))
+    assert str(ei.value) == str(golden("run_E_stiff.npz")["message"])
+
+
+def test_non_native_monitor_rejected():
+    g, d, _ = ring_case()
+    m = P.density_monitor(lambda p: np.ones(p.shape[:-1]), g.extents)
+    with pytest.raises(P.ConfigurationError):
+        P.solve(g, d, m, P.SolverConfig(max_windows=1))
+
+
+@pytest.mark.slow
+def test_c2_two_windows():
+    og, g, d, m, lay, raw = baseline("C2")
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=2, transmission="parallel"))
+    check_run(res, golden("run_C2_parallel_2.npz"), "C2_parallel_2")
+
+
+@pytest.mark.slow
+def test_c4_one_window():
+    og, g, d, m, lay, raw = baseline("C4")
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=1, transmission="parallel"))
+    check_run(res, golden("run_C4_parallel_1.npz"), "C4_parallel_1")
