@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v \
            -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude
 CXXFLAGS := -O2 -fPIC -std=c++17 -ffp-contract=off -Iinclude
 
-OBJ := build/decomp.o build/plan.o build/kernels.o
+OBJ := build/decomp.o build/plan.o build/kernels.o build/persist.o
 
 all: $(OUT)
 
@@ -27,8 +27,11 @@ build/decomp.o: $(SRC)/decomp.cpp $(SRC)/ddpma_internal.h include/ddpma.h | buil
 build/plan.o: $(SRC)/plan.cu $(SRC)/ddpma_internal.h include/ddpma.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/plan.ptxas.log || (cat build/plan.ptxas.log; false)
 
-build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h | build
+build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/kernels.ptxas.log || (cat build/kernels.ptxas.log; false)
+
+build/persist.o: $(SRC)/persist.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh | build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/persist.ptxas.log || (cat build/persist.ptxas.log; false)
 
 $(OUT): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)

@@ -40,11 +40,11 @@ sys.path.insert(0, REPO)
 PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 NCU_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
 
-# SURVEY §8(d) byte model per node-update by kernel class (ddpma.h profile
-# classes): 0 = stage j>=4 (48 B), 1 = stage 2/3, 2 = final eval (48 B),
-# 3 = f0/euler (24 B), 4 = power eval, 5 = mesh/density, 6 = other.
-CLASS_NAMES = ["stage_j>=4", "stage_2_3", "final_eval", "f0_euler", "power_eval",
-               "mesh_density", "other"]
+# Kernel classes of the plan's profiler (ddpma.h): 0 = the fused eval kernel
+# (RKC2 stages, final evals, f0, power iteration; algorithmic bytes per
+# node-update from SURVEY §8(d): 48 B for a stage j>=4), 5 = mesh/density,
+# 6 = other (prologue, traces).
+CLASS_NAMES = ["eval", "unused1", "unused2", "unused3", "unused4", "mesh_density", "other"]
 
 
 def parse():
@@ -309,7 +309,7 @@ def run_gpu(args):
                if traffic_per_node else None)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_eval<2,pow2,STAGEN> (RKC2 stage j>=4: 48 B/node-update)",
+                "kernel": "k_eval<2,pow2> fused RHS+RKC2 stage (48 B/node-update at stage j>=4)",
                 "algo_bytes_per_launch": prof["bytes"][k] / max(1, int(prof["launches"][k])),
                 "avg_launch_ms": prof["ms"][k] / max(1, int(prof["launches"][k])),
                 "share_of_step": round(share, 4), "peak_source": peak_src}

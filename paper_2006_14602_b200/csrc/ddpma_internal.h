@@ -2,6 +2,7 @@
 // (kernels.cu).  Not part of the C ABI.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -24,6 +25,11 @@ constexpr int TY = 8;             // tile height along the next axis
 constexpr int NT = TX * TY;       // threads per CTA
 constexpr int MAXB = 64;          // max Gaussian-mixture bumps
 constexpr int NCLASS = 7;         // profiling kernel classes (ddpma.h)
+// ddpma.h status / scheme values usable in device code
+constexpr int DDPMA_ERR_STIFFNESS_D = 3;
+constexpr int DDPMA_ERR_VALUE_D = 6;
+constexpr int DDPMA_ERR_OVERFLOW_D = 7;
+constexpr int DDPMA_SCHEME_EULER_D = 1;
 
 // Per-axis constants of the uniform global grid (grid.py:37-39) in the exact
 // forms the reference's numpy expressions use.
@@ -72,24 +78,26 @@ struct SubGeo {
   int glo[3];            // global index of the box origin
   int olo[3], ohi[3];    // owned range, box-local inclusive
   long long nodes;
+  int items_x, items_y, items_z, nitems;   // persistent-kernel work items
 };
 
-// One participant (local subdomain) of a batched launch.
+constexpr int IR2 = 32;   // 2D work item: TX x IR2 nodes (each thread IR2/TY rows)
+constexpr int IZ3 = 8;    // 3D work item: TX x TY x IZ3 nodes
+
+// One participant (local subdomain) of a batched launch: its action (mode),
+// buffers and the scalars of that action.
 struct Entry {
   int sub;               // local subdomain index
   int tile_begin;        // first CTA of this entry
   int ntiles;
+  int mode;              // Mode
   int yi, fi;            // current y / f buffer
-  int coef;              // STEP: coefficient table base (index by stage j)
+  int j, s;              // stage index / stages of the step
   int vin, vout;         // POWER: v buffers (-1 = checkerboard seed)
-  int s;                 // stages
-  int pad;
-  double c;              // STEP: h*mu1t | POWER: delta/vnorm | EULER: dtau/m
+  int pad0, pad1;
+  double c;              // STAGE: h*mu1t | POWER: delta/vnorm | EULER: dtau/m
   double h04;            // FINAL: 0.4*h
-};
-
-struct Coef {
-  double mu, nu, hmut, hgt;   // mu_j, nu_j, h*mut_j, h*gt_j
+  double mu, nu, hmut, hgt;   // STAGE j: mu_j, nu_j, h*mut_j, h*gt_j
 };
 
 // Per-local-subdomain results of one round (zeroed / re-initialised each round).
@@ -121,7 +129,8 @@ enum Mode {
   M_FINAL = 4,     // f_new = F(y+d_s), y_new, error ratio max (:177, :204-208)
   M_POWER = 5,     // power-iteration eval (:139-141)
   M_POWER_SEED = 6,// first power-iteration eval from the checkerboard seed
-  M_EULER = 7      // y + (dtau/m)*F(y)                  (:69-74)
+  M_EULER = 7,     // y + (dtau/m)*F(y)                  (:69-74)
+  M_NORM = 8       // sum y^2 (np.linalg.norm(y), :133)
 };
 
 struct KArgs {
@@ -131,12 +140,70 @@ struct KArgs {
   int nent;
   int j;                 // stage index
   Fields F;
-  const Coef* coef;
   SubRes* res;
   double* part;          // per-CTA partial sums
   double* part2;
   const MonitorD* mon;
 };
+
+// Device-resident controller of one local subdomain: the Rkc2Integrator /
+// EulerIntegrator state (integrate.py:109-250) plus the action it currently
+// publishes to the persistent window kernel (persist.cu).
+struct DevCtl {
+  // persistent caches (integrate.py:118-123)
+  int has_sigma, since, interval, has_h;
+  double sigma, h_last;
+  // window state
+  int phase, start_flag, state_flag, rej_row;
+  int flag_rej, s, yi, fi;
+  int ret, sig_k, vin, vout;
+  int euler_left, j, step_flag, pad0;
+  double t, h, delta, vnorm, sig;
+  // failure
+  int fail_status, fail_nonfin, fail_s, fail_yi;
+  int fail_fi, pad1, pad2, pad3;
+  double fail_t, fail_h, fail_h04;
+  // current action (valid for sequence number word >> 32)
+  int a_mode, a_j, a_s, a_yi;
+  int a_fi, a_vin, a_vout, a_pad;
+  double a_c, a_h04, a_mu, a_nu, a_hmut, a_hgt;
+  // per-action accumulators and synchronisation words
+  unsigned int acc_flags, done;
+  unsigned long long acc_emax;
+  unsigned long long word;       // (seq << 32) | claim cursor
+  long long evals;               // RHS evaluations (node-updates / box nodes)
+  double bytes;                  // algorithmic bytes moved
+  unsigned long long t_begin, t_done;   // %globaltimer at window begin / subdomain done
+};
+
+struct TraceRec {
+  int sub, kind, s, flagged, accepted, pad;
+  double h, val;   // kind 0: step (val = emax), kind 1: sigma (val = sigma)
+};
+
+// Arguments of the persistent window kernel.
+struct WinArgs {
+  Prob P;
+  const SubGeo* geo;
+  Fields F;
+  DevCtl* ctl;
+  const int* act;            // active local subdomains
+  int nact;
+  int scheme, substeps, max_stages;
+  double dtau;
+  const double* coef;        // RKC2 tables: coef[4*(off[s]+j)+{0..3}] = mu, nu, mut, gt
+  const int* coef_off;       //   and coef[4*off[s]+0] = mu1t
+  double* part;              // per-item partial sums
+  const long long* poff;     // per local subdomain offset into part
+  unsigned int* n_done;
+  TraceRec* trace;
+  unsigned int* trace_n;
+  int trace_cap;
+};
+
+void launch_window(const WinArgs& a, int nblocks, void* stream);
+int window_blocks(int dim, int pow2);   // co-resident CTAs for the cooperative launch
+void launch_window_begin(const WinArgs& a, void* stream);
 
 struct FaceJob {
   double* dst;
@@ -157,8 +224,7 @@ struct GapJob {
 };
 
 // Launchers (kernels.cu).  All asynchronous on `stream`.
-void launch_eval(int mode, const KArgs& a, int nblocks, void* stream);
-void launch_sumsq(const KArgs& a, int nblocks, void* stream);
+void launch_eval(const KArgs& a, int nblocks, void* stream);
 void launch_finalize(const Entry* ent, int nent, const double* part, SubRes* res,
                      int which, void* stream);
 void launch_mesh(const KArgs& a, int nblocks, int with_residual, void* stream);

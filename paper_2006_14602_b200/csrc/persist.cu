@@ -1,0 +1,884 @@
+// Persistent, device-resident window kernel (sm_100a).
+//
+// One cooperative launch integrates one pseudo-time window for every active
+// local subdomain.  Each subdomain runs its own Rkc2Integrator/Euler state
+// machine (integrate.py:109-250) ON THE DEVICE: its current *action* (f0
+// evaluation, a power-iteration evaluation, RKC2 stage j, the final
+// evaluation with the error ratio, an Euler substep, ||y||) is a pass over
+// all work items (tiles) of its box.  CTAs pull items from any subdomain
+// whose action has unclaimed items (work conserving: a subdomain that needs
+// thousands of stages keeps the whole GPU busy while others are done); the
+// CTA that completes an action's last item reduces its partial sums in a
+// fixed order (deterministic), runs the controller decision on one thread
+// and publishes the next action.
+//
+// Memory ordering: item stores -> __threadfence -> atomicAdd(done); the
+// completing CTA fences before reading partials / controller state (all via
+// L1-bypassing loads).  Publishing writes the action, fences, then swaps the
+// (sequence, cursor) word; a claimer's atomicAdd on that word + fence makes
+// the action and all data of the previous action visible.  Mutable fields are
+// therefore never read through the non-coherent (__ldg) path in this kernel.
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "ddpma_internal.h"
+#include "stencil.cuh"
+
+namespace ddpma {
+
+namespace {
+
+using namespace ddpma::dev;
+
+// Phases of the device controller (same meaning as the host Ctl in plan.cu).
+enum { P_IDLE = 0, P_F0, P_SIG_NORM, P_SIG_ITER, P_STEP, P_EULER, P_DONE, P_FAILED };
+enum { R_START = 0, R_ACCEPT, R_REJECT };
+
+constexpr double kSqrtEps = 1.4901161193847656e-08;   // np.sqrt(np.finfo(float).eps)
+constexpr double kStab = 0.653;                       // integrate.py:36
+constexpr double kMinStep = 1e-14;                    // integrate.py:37
+
+// coherent (L2) loads of mutable data
+__device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
+
+// ------------------------------------------------------------- accessors --
+
+template <int DIM, int YM>
+struct GAcc {   // Y from global memory (boundary nodes), coherent loads
+  const SubGeo* g;
+  const double* y;
+  const double* a;
+  double c;
+  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
+    const long long k = lin<DIM>(*g, i0, i1, i2);
+    const double yv = ldc(y + k);
+    if constexpr (YM == YM_PLAIN) {
+      return yv;
+    } else if constexpr (YM == YM_ADD) {
+      return yv + ldc(a + k);
+    } else if constexpr (YM == YM_SCALED) {
+      return yv + c * ldc(a + k);
+    } else {
+      const int par = (i0 + i1 + (DIM == 3 ? i2 : 0)) & 1;
+      return yv + (par ? -c : c);
+    }
+  }
+};
+
+struct SAcc2 {   // 2D smem tile with a 1-node halo
+  const double* s;
+  int r0, c0;
+  __device__ __forceinline__ double operator()(int i0, int i1, int) const {
+    return s[(i0 - r0 + 1) * (TX + 2) + (i1 - c0 + 1)];
+  }
+};
+
+struct SAcc3 {   // 3D smem tile with a 1-node halo
+  const double* s;
+  int z0, r0, c0;
+  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
+    return s[((i0 - z0 + 1) * (TY + 2) + (i1 - r0 + 1)) * (TX + 2) + (i2 - c0 + 1)];
+  }
+};
+
+struct Act {      // the action of the claimed item (broadcast through smem)
+  int mode, j, s, yi, fi, vin, vout, sub;
+  double c, h04, mu, nu, hmut, hgt;
+};
+
+struct Acc {      // per-thread accumulators over the thread's nodes
+  unsigned flag, nonfin;
+  double ratio, psum;
+};
+
+template <int YM>
+__device__ __forceinline__ double ymake(double yv, double av, double c, int par) {
+  if constexpr (YM == YM_PLAIN) {
+    return yv;
+  } else if constexpr (YM == YM_ADD) {
+    return yv + av;
+  } else if constexpr (YM == YM_SCALED) {
+    return yv + c * av;
+  } else {
+    return yv + (par ? -c : c);
+  }
+}
+
+// One node: RHS (pma_rhs_frozen) + the consuming epilogue of the action.
+template <int DIM, bool P2, int MODE, int YM, class SA>
+__device__ __forceinline__ void node(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
+                                     int i1, int i2, const SA& S, const double* aptr, Acc& acc) {
+  const long long k = lin<DIM>(g, i0, i1, i2);
+  const double* yb = A.F.y[t.yi];
+  if constexpr (MODE == M_NORM) {
+    const double y = ldc(yb + k);
+    acc.psum += y * y;
+    return;
+  } else {
+    const bool dir = dirichlet<DIM>(g, i0, i1, i2);
+    bool interior = i0 >= 1 && i0 <= g.n[0] - 2 && i1 >= 1 && i1 <= g.n[1] - 2;
+    if constexpr (DIM == 3) interior = interior && i2 >= 1 && i2 <= g.n[2] - 2;
+    double det;
+    if (interior) det = hdet<DIM, P2>(A.P, g, i0, i1, i2, S);
+    else det = hdet<DIM, P2>(A.P, g, i0, i1, i2, GAcc<DIM, YM>{&g, yb, aptr, t.c});
+    const double F = dir ? 0.0 : logequi(ldc(A.F.mr + k), det, A.P.guard, A.P.floor);
+    acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
+    if constexpr (MODE == M_F0) {
+      A.F.f[t.fi][k] = F;
+    } else if constexpr (MODE == M_EULER) {
+      A.F.y[1 - t.yi][k] = ldc(yb + k) + t.c * F;
+    } else if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
+      const double f0 = ldc(A.F.f[t.fi] + k);
+      const double d1 = t.c * f0;
+      double dp, dp2;
+      if constexpr (MODE == M_STAGE2) {
+        dp = d1;
+        dp2 = 0.0;
+      } else if constexpr (MODE == M_STAGE3) {
+        dp = ldc(A.F.d[2] + k);
+        dp2 = d1;
+      } else {
+        dp = ldc(A.F.d[(t.j - 1) % 3] + k);
+        dp2 = ldc(A.F.d[(t.j - 2) % 3] + k);
+      }
+      A.F.d[t.j % 3][k] = ((t.mu * dp + t.nu * dp2) + t.hmut * F) + t.hgt * f0;
+    } else if constexpr (MODE == M_FINAL) {
+      const double ds = ldc(A.F.d[t.s % 3] + k);
+      const double yv = ldc(yb + k);
+      const double yn = yv + ds;
+      const double f0 = ldc(A.F.f[t.fi] + k);
+      A.F.f[1 - t.fi][k] = F;
+      A.F.y[1 - t.yi][k] = yn;
+      const double err = -0.8 * ds + t.h04 * (f0 + F);
+      const double ay = fabs(yv), an = fabs(yn);
+      const double mx = (ay >= an || isnan(ay)) ? ay : an;
+      const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
+      if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
+      else acc.nonfin = 1;
+    } else {
+      const double diff = F - ldc(A.F.f[t.fi] + k);
+      A.F.d[t.vout][k] = diff;
+      acc.psum += diff * diff;
+    }
+  }
+}
+
+// Interior 2D Hessian determinant straight from the smem tile: the interior
+// formulas of hessian_det_fd (pma.py:87-140, np.gradient interior) in the
+// same evaluation order as hdet's interior branch (bitwise identical).
+template <bool P2>
+__device__ __forceinline__ double hdet2_fast(const Prob& P, const double* p) {
+  constexpr int W = TX + 2;
+  const double c = p[0];
+  const double h00 = dv<P2>((p[W] - 2.0 * c) + p[-W], P.ax[0].hh, P.ax[0].ihh);
+  const double h11 = dv<P2>((p[1] - 2.0 * c) + p[-1], P.ax[1].hh, P.ax[1].ihh);
+  const double gp = dv<P2>(p[W + 1] - p[W - 1], P.ax[1].twoh, P.ax[1].itwoh);
+  const double gm = dv<P2>(p[-W + 1] - p[-W - 1], P.ax[1].twoh, P.ax[1].itwoh);
+  const double h01 = dv<P2>(gp - gm, P.ax[0].twoh, P.ax[0].itwoh);
+  return h00 * h11 - h01 * h01;
+}
+
+// One 2D work item: TX x IR2 nodes, each thread IR2/TY rows.  Center values
+// are prefetched first, then the tile + halo of Y is staged in smem, then the
+// nodes are evaluated (interior: smem stencil; box faces: generic path).
+template <bool P2, int MODE, int YM>
+__device__ void item2(const WinArgs& A, const SubGeo& g, const Act& t, int item, double* sY,
+                      Acc& acc) {
+  constexpr int W = TX + 2, H = IR2 + 2, R = IR2 / TY;
+  const int ix = item % g.items_x, iy = item / g.items_x;
+  const int c0 = ix * TX, r0 = iy * IR2;
+  const int n0 = g.n[0], n1 = g.n[1];
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  constexpr bool NEED_F0 = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN ||
+                           MODE == M_FINAL || MODE == M_POWER || MODE == M_POWER_SEED;
+  constexpr bool NEED_Y = MODE == M_FINAL || MODE == M_EULER || MODE == M_NORM;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  const int i1 = c0 + threadIdx.x;
+  double cm[R], cf[R], cd[R], cd2[R], cy[R];
+  bool ok[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i0 = r0 + threadIdx.y + q * TY;
+    ok[q] = i1 < n1 && i0 < n0;
+    cm[q] = cf[q] = cd[q] = cd2[q] = cy[q] = 0.0;
+    if (ok[q]) {
+      const long long k = g.off + (long long)i0 * g.pitch + i1;
+      if constexpr (MODE != M_NORM) cm[q] = ldc(A.F.mr + k);
+      if constexpr (NEED_F0) cf[q] = ldc(A.F.f[t.fi] + k);
+      if constexpr (MODE == M_STAGE3) cd[q] = ldc(A.F.d[2] + k);
+      if constexpr (MODE == M_STAGEN) {
+        cd[q] = ldc(A.F.d[(t.j - 1) % 3] + k);
+        cd2[q] = ldc(A.F.d[(t.j - 2) % 3] + k);
+      }
+      if constexpr (MODE == M_FINAL) cd[q] = ldc(A.F.d[t.s % 3] + k);
+      if constexpr (NEED_Y) cy[q] = ldc(yb + k);
+    }
+  }
+  if constexpr (MODE != M_NORM) {
+#pragma unroll
+    for (int it = 0; it < (W * H + NT - 1) / NT; ++it) {
+      const int e = tid + it * NT;
+      if (e < W * H) {
+        const int rr = e / W, cc = e - rr * W;
+        const int i0 = r0 - 1 + rr, j1 = c0 - 1 + cc;
+        double v = 0.0;
+        if (i0 >= 0 && i0 < n0 && j1 >= 0 && j1 < n1) {
+          const long long k = g.off + (long long)i0 * g.pitch + j1;
+          const double av = (YM == YM_ADD || YM == YM_SCALED) ? ldc(ap + k) : 0.0;
+          v = ymake<YM>(ldc(yb + k), av, t.c, (i0 + j1) & 1);
+        }
+        sY[e] = v;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    if (!ok[q]) continue;
+    const int i0 = r0 + threadIdx.y + q * TY;
+    const long long k = g.off + (long long)i0 * g.pitch + i1;
+    if constexpr (MODE == M_NORM) {
+      acc.psum += cy[q] * cy[q];
+    } else {
+      const bool dir = dirichlet<2>(g, i0, i1, 0);
+      const bool interior = i0 >= 1 && i0 <= n0 - 2 && i1 >= 1 && i1 <= n1 - 2;
+      double det;
+      if (interior) det = hdet2_fast<P2>(A.P, sY + (threadIdx.y + q * TY + 1) * W + threadIdx.x + 1);
+      else det = hdet<2, P2>(A.P, g, i0, i1, 0, GAcc<2, YM>{&g, yb, ap, t.c});
+      const double F = dir ? 0.0 : logequi(cm[q], det, A.P.guard, A.P.floor);
+      acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
+      if constexpr (MODE == M_F0) {
+        A.F.f[t.fi][k] = F;
+      } else if constexpr (MODE == M_EULER) {
+        A.F.y[1 - t.yi][k] = cy[q] + t.c * F;
+      } else if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
+        const double f0 = cf[q];
+        const double d1 = t.c * f0;
+        double dp, dp2;
+        if constexpr (MODE == M_STAGE2) {
+          dp = d1;
+          dp2 = 0.0;
+        } else if constexpr (MODE == M_STAGE3) {
+          dp = cd[q];
+          dp2 = d1;
+        } else {
+          dp = cd[q];
+          dp2 = cd2[q];
+        }
+        A.F.d[t.j % 3][k] = ((t.mu * dp + t.nu * dp2) + t.hmut * F) + t.hgt * f0;
+      } else if constexpr (MODE == M_FINAL) {
+        const double ds = cd[q], yv = cy[q], f0 = cf[q];
+        const double yn = yv + ds;
+        A.F.f[1 - t.fi][k] = F;
+        A.F.y[1 - t.yi][k] = yn;
+        const double err = -0.8 * ds + t.h04 * (f0 + F);
+        const double ay = fabs(yv), an = fabs(yn);
+        const double mx = (ay >= an || isnan(ay)) ? ay : an;
+        const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
+        if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
+        else acc.nonfin = 1;
+      } else {
+        const double diff = F - cf[q];
+        A.F.d[t.vout][k] = diff;
+        acc.psum += diff * diff;
+      }
+    }
+  }
+}
+
+// One 3D work item: TX x TY x IZ3 nodes; tile + halo staged in smem.
+template <bool P2, int MODE, int YM>
+__device__ void item3(const WinArgs& A, const SubGeo& g, const Act& t, int item, double* sY,
+                      Acc& acc) {
+  const int ix = item % g.items_x;
+  const int r = item / g.items_x;
+  const int iy = r % g.items_y, iz = r / g.items_y;
+  const int c0 = ix * TX, r0 = iy * TY, z0 = iz * IZ3;
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  if constexpr (MODE != M_NORM) {
+    constexpr int W = TX + 2, H = TY + 2, D = IZ3 + 2;
+    for (int e = tid; e < W * H * D; e += NT) {
+      const int cc = e % W, rr = (e / W) % H, zz = e / (W * H);
+      const int i0 = z0 - 1 + zz, i1 = r0 - 1 + rr, i2 = c0 - 1 + cc;
+      double v = 0.0;
+      if (i0 >= 0 && i0 < g.n[0] && i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2]) {
+        const long long k = g.off + ((long long)i0 * g.n[1] + i1) * g.pitch + i2;
+        const double av = (YM == YM_ADD || YM == YM_SCALED) ? ldc(ap + k) : 0.0;
+        v = ymake<YM>(ldc(yb + k), av, t.c, (i0 + i1 + i2) & 1);
+      }
+      sY[e] = v;
+    }
+    __syncthreads();
+  }
+  const SAcc3 S{sY, z0, r0, c0};
+  const int i2 = c0 + threadIdx.x, i1 = r0 + threadIdx.y;
+  if (i1 < g.n[1] && i2 < g.n[2]) {
+    for (int q = 0; q < IZ3; ++q) {
+      const int i0 = z0 + q;
+      if (i0 < g.n[0]) node<3, P2, MODE, YM>(A, g, t, i0, i1, i2, S, ap, acc);
+    }
+  }
+}
+
+template <int DIM, bool P2, int MODE, int YM>
+__device__ __forceinline__ void run_item(const WinArgs& A, const SubGeo& g, const Act& t, int item,
+                                         double* sY, Acc& acc) {
+  if constexpr (DIM == 2) item2<P2, MODE, YM>(A, g, t, item, sY, acc);
+  else item3<P2, MODE, YM>(A, g, t, item, sY, acc);
+}
+
+template <int DIM, bool P2>
+__device__ void dispatch_item(const WinArgs& A, const SubGeo& g, const Act& t, int item,
+                              double* sY, Acc& acc) {
+  switch (t.mode) {
+    case M_F0: run_item<DIM, P2, M_F0, YM_PLAIN>(A, g, t, item, sY, acc); break;
+    case M_EULER: run_item<DIM, P2, M_EULER, YM_PLAIN>(A, g, t, item, sY, acc); break;
+    case M_STAGE2: run_item<DIM, P2, M_STAGE2, YM_SCALED>(A, g, t, item, sY, acc); break;
+    case M_STAGE3: run_item<DIM, P2, M_STAGE3, YM_ADD>(A, g, t, item, sY, acc); break;
+    case M_STAGEN: run_item<DIM, P2, M_STAGEN, YM_ADD>(A, g, t, item, sY, acc); break;
+    case M_FINAL: run_item<DIM, P2, M_FINAL, YM_ADD>(A, g, t, item, sY, acc); break;
+    case M_POWER: run_item<DIM, P2, M_POWER, YM_SCALED>(A, g, t, item, sY, acc); break;
+    case M_POWER_SEED: run_item<DIM, P2, M_POWER_SEED, YM_SEED>(A, g, t, item, sY, acc); break;
+    case M_NORM: run_item<DIM, P2, M_NORM, YM_PLAIN>(A, g, t, item, sY, acc); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ double mode_bytes_d(int mode) {
+  switch (mode) {
+    case M_F0: return 24.0;
+    case M_STAGE2: return 32.0;
+    case M_STAGE3: return 40.0;
+    case M_STAGEN: return 48.0;
+    case M_FINAL: return 48.0;
+    case M_POWER: return 40.0;
+    case M_POWER_SEED: return 32.0;
+    case M_EULER: return 24.0;
+    case M_NORM: return 8.0;
+    default: return 0.0;
+  }
+}
+
+// ------------------------------------------------- device controller --------
+// Runs on ONE thread (thread 0 of the CTA completing an action) on a private
+// copy of the subdomain's DevCtl.  Statement for statement the host Ctl logic
+// of plan.cu, i.e. integrate.py:180-250.
+
+__device__ void trace_rec(const WinArgs& A, int gid, int kind, double h, int s, double v, int fl,
+                          int acc) {
+  if (A.trace == nullptr) return;
+  const unsigned i = atomicAdd(A.trace_n, 1u);
+  if ((int)i < A.trace_cap) A.trace[i] = TraceRec{gid, kind, s, fl, acc, 0, h, v};
+}
+
+__device__ void d_loop_check(const WinArgs& A, DevCtl& c);
+
+__device__ void d_fail(DevCtl& c, int status) {
+  c.phase = P_FAILED;
+  c.fail_status = status;
+  c.fail_t = c.t;
+  c.fail_h = c.h;
+  c.fail_s = c.s;
+  c.fail_yi = c.yi;
+  c.fail_fi = c.fi;
+  c.fail_h04 = 0.4 * c.h;
+}
+
+__device__ void d_prepare_step(const WinArgs& A, DevCtl& c) {   // integrate.py:198-202
+  const double total = A.dtau;
+  const int ms = A.max_stages;
+  const double rem = total - c.t;
+  c.h = rem < c.h ? rem : c.h;
+  const double cap = kStab * (double)((long long)ms * ms);
+  if (c.sigma > 0.0 && c.h * c.sigma > cap) c.h = cap / c.sigma;
+  const double hs = c.h * c.sigma;
+  long long s;
+  if (hs <= 0.0) {
+    s = 2;
+  } else {
+    const double v = ceil(sqrt(1.05 * hs / kStab));
+    if (isnan(v)) {
+      d_fail(c, DDPMA_ERR_VALUE_D);
+      return;
+    }
+    if (isinf(v)) {
+      d_fail(c, DDPMA_ERR_OVERFLOW_D);
+      return;
+    }
+    s = v > 1e9 ? 1000000000LL : (long long)v;
+    s = s < 2 ? 2 : s;
+  }
+  c.s = (int)(s < ms ? s : ms);
+  c.j = 0;
+  c.phase = P_STEP;
+}
+
+__device__ void d_after_start(const WinArgs& A, DevCtl& c) {    // integrate.py:187-196
+  const double total = A.dtau;
+  double h;
+  if (c.sigma <= 0.0) {
+    h = total;
+  } else {
+    const double lo = 10.0 * kMinStep * total, q = 0.25 / c.sigma;
+    const double mx = lo < q ? q : lo;           // max(lo, q)
+    h = mx < total ? mx : total;                 // min(total, .)
+  }
+  if (c.has_h) h = c.h_last < total ? c.h_last : total;
+  c.h = h;
+  c.t = 0.0;
+  c.state_flag = c.start_flag;
+  c.rej_row = 0;
+  c.flag_rej = 0;
+  d_loop_check(A, c);
+}
+
+__device__ void d_loop_check(const WinArgs& A, DevCtl& c) {     // integrate.py:197
+  if (c.t < A.dtau * (1.0 - 1e-13)) d_prepare_step(A, c);
+  else c.phase = P_DONE;
+}
+
+__device__ void d_finish_sigma(const WinArgs& A, DevCtl& c, int gid) {   // :147-153
+  c.since = 0;
+  if (c.has_sigma && c.sig <= 1.05 * c.sigma / 1.2) c.interval = 2 * c.interval < 500 ? 2 * c.interval : 500;
+  else c.interval = 25;
+  c.sigma = 1.2 * c.sig;
+  c.has_sigma = 1;
+  trace_rec(A, gid, 1, 0.0, 0, c.sigma, 0, 0);
+  if (c.ret == R_START) d_after_start(A, c);
+  else d_loop_check(A, c);
+}
+
+__device__ void d_start_sigma(DevCtl& c, int ret) {
+  c.ret = ret;
+  c.phase = P_SIG_NORM;
+}
+
+// The action `a_mode` of this subdomain has completed; decide.
+__device__ void d_complete(const WinArgs& A, DevCtl& c, int l, double sum, long long nodes) {
+  const double total = A.dtau;
+  const int gid = A.geo[l].gid;
+  const int mode = c.a_mode;
+  c.bytes += mode_bytes_d(mode) * (double)nodes;
+  if (mode != M_NORM) c.evals += 1;
+  switch (mode) {
+    case M_STAGE2:
+    case M_STAGE3:
+    case M_STAGEN:
+      c.step_flag |= (c.acc_flags & 1u) ? 1 : 0;
+      c.j += 1;
+      break;
+    case M_F0:
+      c.start_flag = (c.acc_flags & 1u) ? 1 : 0;
+      if (!c.has_sigma || c.since >= c.interval) d_start_sigma(c, R_START);
+      else d_after_start(A, c);
+      break;
+    case M_NORM: {                              // integrate.py:132-133
+      c.delta = kSqrtEps * (1.0 + sqrt(sum));
+      c.sig = 0.0;
+      c.sig_k = 0;
+      c.vin = -1;
+      c.vnorm = sqrt((double)nodes);
+      if (c.vnorm == 0.0) d_finish_sigma(A, c, gid);
+      else c.phase = P_SIG_ITER;
+      break;
+    }
+    case M_POWER:
+    case M_POWER_SEED: {                        // integrate.py:135-146
+      const double nrm = sqrt(sum);
+      const double ns = nrm / c.delta;
+      c.vin = c.vout;
+      c.sig_k += 1;
+      if (c.sig > 0.0 && fabs(ns - c.sig) <= 0.01 * ns) {
+        c.sig = ns;
+        d_finish_sigma(A, c, gid);
+        break;
+      }
+      c.sig = ns;
+      if (c.sig_k >= 20) {
+        d_finish_sigma(A, c, gid);
+        break;
+      }
+      c.vnorm = nrm;
+      if (c.vnorm == 0.0) d_finish_sigma(A, c, gid);
+      break;
+    }
+    case M_FINAL: {                             // integrate.py:203-249
+      const bool nonfin = (c.acc_flags & 4u) != 0;
+      const bool flagged = c.step_flag || (c.acc_flags & 3u) != 0;
+      const bool end_flag = (c.acc_flags & 2u) != 0;
+      const double emax = __longlong_as_double((long long)c.acc_emax);
+      const bool flag_fail = flagged && !c.state_flag && c.flag_rej < 8;
+      const bool bad = flag_fail || nonfin;
+      const bool ok = !bad && emax <= 1.0;
+      trace_rec(A, gid, 0, c.h, c.s, nonfin ? __longlong_as_double(0x7ff8000000000000LL) : emax,
+                flagged ? 1 : 0, ok ? 1 : 0);
+      c.j = 0;
+      if (ok) {
+        c.t += c.h;
+        c.yi ^= 1;
+        c.fi ^= 1;
+        c.state_flag = end_flag ? 1 : 0;
+        c.since += 1;
+        c.rej_row = 0;
+        const bool need = c.since >= c.interval && c.t < total;
+        double grow = 5.0;
+        if (emax != 0.0) {
+          const double gg = 0.8 * pow(emax, -1.0 / 3.0);
+          grow = gg < 5.0 ? gg : 5.0;
+        }
+        c.h = c.h * (0.1 < grow ? grow : 0.1);
+        c.h_last = c.h;
+        c.has_h = 1;
+        if (need) d_start_sigma(c, R_ACCEPT);
+        else d_loop_check(A, c);
+      } else {
+        if (flag_fail) {
+          c.flag_rej += 1;
+          c.h *= 0.5;
+        } else if (nonfin) {
+          c.h *= 0.5;
+          c.rej_row += 1;
+        } else {
+          const double gg = 0.8 * pow(emax, -1.0 / 3.0);
+          c.h *= (0.1 < gg ? gg : 0.1);
+          c.rej_row += 1;
+        }
+        const bool need = c.rej_row >= 2;
+        if (need) c.rej_row = 0;
+        if (c.h < kMinStep * total || c.flag_rej + c.rej_row > 60) {
+          d_fail(c, DDPMA_ERR_STIFFNESS_D);
+          c.fail_nonfin = nonfin ? 1 : 0;
+          break;
+        }
+        if (need) d_start_sigma(c, R_REJECT);
+        else d_loop_check(A, c);
+      }
+      break;
+    }
+    case M_EULER:                               // integrate.py:69-74
+      c.yi ^= 1;
+      if (--c.euler_left == 0) c.phase = P_DONE;
+      break;
+    default:
+      break;
+  }
+}
+
+// Fill the action fields from the phase (the next action of the subdomain).
+// Returns false when the subdomain has finished (DONE / FAILED).
+__device__ bool d_next_action(const WinArgs& A, DevCtl& c) {
+  c.a_yi = c.yi;
+  c.a_fi = c.fi;
+  c.a_s = c.s;
+  switch (c.phase) {
+    case P_F0:
+      c.a_mode = M_F0;
+      return true;
+    case P_SIG_NORM:
+      c.a_mode = M_NORM;
+      return true;
+    case P_SIG_ITER:
+      c.a_mode = c.vin < 0 ? M_POWER_SEED : M_POWER;
+      c.a_vin = c.vin;
+      c.vout = c.vin < 0 ? 0 : 1 - c.vin;
+      c.a_vout = c.vout;
+      c.a_c = c.delta / c.vnorm;
+      return true;
+    case P_STEP: {
+      if (c.j == 0) {
+        c.j = 2;
+        c.step_flag = 0;
+      }
+      const int base = A.coef_off[c.s];
+      c.a_c = c.h * A.coef[4 * base + 0];      // h * mu1_t
+      if (c.j <= c.s) {
+        const int j = c.j;
+        c.a_mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
+        c.a_j = j;
+        c.a_mu = A.coef[4 * (base + j) + 0];
+        c.a_nu = A.coef[4 * (base + j) + 1];
+        c.a_hmut = c.h * A.coef[4 * (base + j) + 2];
+        c.a_hgt = c.h * A.coef[4 * (base + j) + 3];
+      } else {
+        c.a_mode = M_FINAL;
+        c.a_h04 = 0.4 * c.h;
+      }
+      return true;
+    }
+    case P_EULER:
+      c.a_mode = M_EULER;
+      c.a_c = A.dtau / (double)A.substeps;
+      return true;
+    default:
+      return false;
+  }
+}
+
+__device__ __forceinline__ void ctl_load(DevCtl& dst, const DevCtl* src) {
+  long long* d = reinterpret_cast<long long*>(&dst);
+  const long long* s = reinterpret_cast<const long long*>(src);
+#pragma unroll 4
+  for (int i = 0; i < (int)(sizeof(DevCtl) / 8); ++i) d[i] = __ldcg(s + i);
+}
+
+__device__ __forceinline__ void ctl_store(DevCtl* dst, const DevCtl& src) {
+  long long* d = reinterpret_cast<long long*>(dst);
+  const long long* s = reinterpret_cast<const long long*>(&src);
+  // never overwrite the synchronisation word here (published separately)
+  const int wi = (int)(offsetof(DevCtl, word) / 8);
+#pragma unroll 4
+  for (int i = 0; i < (int)(sizeof(DevCtl) / 8); ++i)
+    if (i != wi) __stcg(d + i, s[i]);
+}
+
+// Publish the next action of subdomain l from the private copy c (thread 0).
+__device__ void d_publish(const WinArgs& A, DevCtl& c, DevCtl* gc) {
+  const unsigned long long seq = (c.word >> 32) + 1;
+  const bool more = d_next_action(A, c);
+  c.acc_flags = 0;
+  c.acc_emax = 0ull;
+  c.done = 0;
+  ctl_store(gc, c);
+  __threadfence();
+  if (more) {
+    atomicExch(&gc->word, seq << 32);
+  } else {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    __stcg(reinterpret_cast<long long*>(&gc->t_done), (long long)now);
+    atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+    atomicAdd(A.n_done, 1u);
+  }
+}
+
+__device__ __forceinline__ double block_sum2(double v, double* sh) {
+  return block_sum(v, sh);
+}
+
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A) {
+  constexpr int SM_ELEMS = DIM == 2 ? (TX + 2) * (IR2 + 2) : (TX + 2) * (TY + 2) * (IZ3 + 2);
+  __shared__ double sY[SM_ELEMS];
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_max[NT / 32];
+  __shared__ Act s_act;
+  __shared__ DevCtl s_ctl;
+  __shared__ int s_sub, s_item, s_exit, s_last;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  unsigned backoff = 32;
+  while (true) {
+    // Warp 0 claims the next item: subdomains are scanned in PRIORITY order
+    // (A.act is sorted by the previous window's work, the straggler first),
+    // 32 candidates per round in parallel; the first claimable one wins.
+    if (threadIdx.y == 0) {
+      const int lane = threadIdx.x;
+      int got = -1, item = 0;
+      for (int base = 0; base < A.nact && got < 0; base += 32) {
+        const int q = base + lane;
+        int l = -1;
+        bool claimable = false;
+        if (q < A.nact) {
+          l = A.act[q];
+          const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
+          claimable = (unsigned)(w & 0xffffffffull) < (unsigned)A.geo[l].nitems;
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, claimable);
+        while (mask != 0u && got < 0) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1u;
+          int it = -1;
+          if (lane == src) {
+            const unsigned long long w2 = atomicAdd(&A.ctl[l].word, 1ull);
+            const unsigned u = (unsigned)(w2 & 0xffffffffull);
+            if (u < (unsigned)A.geo[l].nitems) it = (int)u;
+          }
+          it = __shfl_sync(0xffffffffu, it, src);
+          if (it >= 0) {
+            got = __shfl_sync(0xffffffffu, l, src);
+            item = it;
+          }
+        }
+      }
+      if (lane == 0) {
+        s_sub = got;
+        s_item = item;
+        s_exit = 0;
+        if (got < 0) {
+          s_exit = *(volatile unsigned*)A.n_done >= (unsigned)A.nact;
+        } else {
+          __threadfence();   // acquire: the action and the previous action's data
+          const DevCtl* gc = A.ctl + got;
+          Act t;
+          t.mode = __ldcg(&gc->a_mode);
+          t.j = __ldcg(&gc->a_j);
+          t.s = __ldcg(&gc->a_s);
+          t.yi = __ldcg(&gc->a_yi);
+          t.fi = __ldcg(&gc->a_fi);
+          t.vin = __ldcg(&gc->a_vin);
+          t.vout = __ldcg(&gc->a_vout);
+          t.sub = got;
+          t.c = __ldcg(&gc->a_c);
+          t.h04 = __ldcg(&gc->a_h04);
+          t.mu = __ldcg(&gc->a_mu);
+          t.nu = __ldcg(&gc->a_nu);
+          t.hmut = __ldcg(&gc->a_hmut);
+          t.hgt = __ldcg(&gc->a_hgt);
+          s_act = t;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_sub < 0) {
+      if (s_exit) break;
+      if (tid == 0) __nanosleep(backoff);
+      backoff = backoff < 256 ? backoff * 2 : 256;
+      __syncthreads();
+      continue;
+    }
+    backoff = 32;
+    const Act t = s_act;
+    const int l = t.sub;
+    const SubGeo& g = A.geo[l];
+    Acc acc{0u, 0u, 0.0, 0.0};
+    dispatch_item<DIM, P2>(A, g, t, s_item, sY, acc);
+    // CTA reductions of the item
+    const int any = __syncthreads_or(acc.flag);
+    const int anynf = __syncthreads_or(acc.nonfin);
+    unsigned long long emax = 0ull;
+    if (t.mode == M_FINAL)
+      emax = block_max_u64((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
+    double psum = 0.0;
+    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
+    if (sums) psum = block_sum2(acc.psum, sh_sum);
+    if (tid == 0) {
+      DevCtl* gc = A.ctl + l;
+      if (sums) __stcg(A.part + A.poff[l] + s_item, psum);
+      unsigned bits = 0;
+      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
+      if (anynf) bits |= 4u;
+      if (bits) atomicOr(&gc->acc_flags, bits);
+      if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
+      __threadfence();
+      const unsigned d = atomicAdd(&gc->done, 1u);
+      s_last = d == (unsigned)g.nitems - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      double sum = 0.0;
+      if (sums) {   // fixed-order reduction of the item partials (deterministic)
+        double v = 0.0;
+        for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
+        sum = block_sum2(v, sh_sum);
+      }
+      if (threadIdx.y == 0) {   // warp 0: controller state in/out in parallel
+        DevCtl* gc = A.ctl + l;
+        constexpr int NW = (int)(sizeof(DevCtl) / 8);
+        constexpr int WI = (int)(offsetof(DevCtl, word) / 8);
+        long long* sc = reinterpret_cast<long long*>(&s_ctl);
+        const long long* gsrc = reinterpret_cast<const long long*>(gc);
+        for (int i = threadIdx.x; i < NW; i += 32) sc[i] = __ldcg(gsrc + i);
+        __syncwarp();
+        bool more = false;
+        unsigned long long seq = 0;
+        if (threadIdx.x == 0) {
+          d_complete(A, s_ctl, l, sum, g.nodes);
+          seq = (s_ctl.word >> 32) + 1;
+          more = d_next_action(A, s_ctl);
+          s_ctl.acc_flags = 0;
+          s_ctl.acc_emax = 0ull;
+          s_ctl.done = 0;
+          if (!more) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            s_ctl.t_done = now;
+          }
+        }
+        __syncwarp();
+        long long* gdst = reinterpret_cast<long long*>(gc);
+        for (int i = threadIdx.x; i < NW; i += 32)
+          if (i != WI) __stcg(gdst + i, sc[i]);
+        __syncwarp();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          if (more) {
+            atomicExch(&gc->word, seq << 32);
+          } else {
+            atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+            atomicAdd(A.n_done, 1u);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Window start for the active subdomains (one thread each): phase F0 /
+// EULER, first action published.
+__global__ void k_window_begin(const WinArgs A) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= A.nact) return;
+  const int l = A.act[q];
+  DevCtl* gc = A.ctl + l;
+  DevCtl c;
+  ctl_load(c, gc);
+  c.fail_status = 0;
+  c.j = 0;
+  if (A.scheme == DDPMA_SCHEME_EULER_D) {
+    c.phase = P_EULER;
+    c.euler_left = A.substeps;
+  } else {
+    c.phase = P_F0;
+  }
+  c.word = (c.word & 0xffffffff00000000ull);
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c.t_begin));
+  d_publish(A, c, gc);
+}
+
+}  // namespace
+
+int window_blocks(int dim, int pow2) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dim == 2) {
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<2, true>, NT, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<2, false>, NT, 0);
+  } else {
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, true>, NT, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, false>, NT, 0);
+  }
+  return sms * (per > 0 ? per : 1);
+}
+
+void launch_window_begin(const WinArgs& a, void* stream) {
+  if (a.nact <= 0) return;
+  k_window_begin<<<(a.nact + 63) / 64, 64, 0, (cudaStream_t)stream>>>(a);
+}
+
+void launch_window(const WinArgs& a, int nb, void* stream) {
+  if (a.nact <= 0) return;
+  const dim3 blk(TX, TY);
+  void* args[] = {(void*)&a};
+  void* fn;
+  if (a.P.dim == 2) fn = a.P.pow2 ? (void*)k_window<2, true> : (void*)k_window<2, false>;
+  else fn = a.P.pow2 ? (void*)k_window<3, true> : (void*)k_window<3, false>;
+  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, 0, (cudaStream_t)stream);
+}
+
+}  // namespace ddpma

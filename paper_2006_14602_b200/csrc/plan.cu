@@ -60,6 +60,10 @@ struct Ctl {
   int sig_k = 0, vin = -1, vout = 0;
   // euler
   int euler_left = 0;
+  // pipeline
+  bool waiting = false;   // an issued action needs its result before the next one
+  int j_next = 0;         // next stage of the current step (0 = step not started)
+  bool step_flag = false; // OR of the stage positivity flags of the current step
 };
 
 struct Failure {
@@ -158,6 +162,34 @@ struct ddpma_plan {
   bool exch_ready = false;
   struct Seg { int recv_gid, axis, side, donor_gid; long long off; int ext0, ext1; };
   std::vector<Seg> send_segs, recv_segs;   // send_segs: offsets into the send buffer
+  // asynchronous launch pipeline (advance_set): per-slot entries/results
+  static constexpr int R = 4;
+  Entry* h_ent[R] = {};
+  Entry* d_ent[R] = {};
+  SubRes* d_ring = nullptr;
+  SubRes* h_ring = nullptr;
+  double* d_partring = nullptr;
+  cudaEvent_t ring_ev[R] = {};
+  long long kissue = 0;
+  std::vector<RkcCoeffs> coeff_cache;       // index s (lru_cache of _rkc_coeffs)
+  // device-resident controller (persist.cu)
+  DevCtl* d_ctl = nullptr;
+  DevCtl* h_ctl = nullptr;
+  std::vector<DevCtl> ctl_prev;            // counters at the previous read-back
+  double* d_coef = nullptr;
+  int* d_coef_off = nullptr;
+  double* d_part_items = nullptr;
+  long long* d_poff = nullptr;
+  int* d_act = nullptr;
+  int* h_act = nullptr;
+  unsigned int* d_ndone = nullptr;
+  TraceRec* d_trace = nullptr;
+  unsigned int* d_trace_n = nullptr;
+  int trace_cap = 0;
+  int win_blocks = 0;
+  bool host_ctl = false;
+  std::vector<long long> last_evals;       // per local subdomain, previous window
+  long long mode_nodes[9] = {0};
 };
 
 namespace {
@@ -290,28 +322,89 @@ long long entries_nodes(ddpma_plan* p, const Entry* ents, int n) {
   return s;
 }
 
-ddpma_status eval_launch(ddpma_plan* p, int mode, const Entry* d_ents, const Entry* h_ents,
-                         int nent, int nblocks, int j, const Coef* d_coef, int klass, double bpn) {
+ddpma_status sync(ddpma_plan* p);
+
+// SURVEY §8(d) algorithmic bytes per node-update of each action.
+double mode_bytes(int mode) {
+  switch (mode) {
+    case M_F0: return 24.0;        // y, mr -> f0
+    case M_STAGE2: return 32.0;    // y, f0, mr -> d2
+    case M_STAGE3: return 40.0;    // y, d2, f0, mr -> d3
+    case M_STAGEN: return 48.0;    // y, d_{j-1}, d_{j-2}, f0, mr -> d_j
+    case M_FINAL: return 48.0;     // y, d_s, f0, mr -> f_new, y_new
+    case M_POWER: return 40.0;     // y, v, f0, mr -> v'
+    case M_POWER_SEED: return 32.0;
+    case M_EULER: return 24.0;     // y, mr -> y_new
+    case M_NORM: return 8.0;
+    default: return 0.0;
+  }
+}
+
+const RkcCoeffs& coeffs(ddpma_plan* p, int s) {
+  if ((int)p->coeff_cache.size() <= s) p->coeff_cache.resize(s + 1);
+  RkcCoeffs& c = p->coeff_cache[s];
+  if (c.mu.empty()) rkc_coeffs(s, c);
+  return c;
+}
+
+// Enqueue one mixed eval launch over `ents` into result slot `slot`:
+// reset slot, copy entries, kernel, (finalize sums), D2H results, event.
+ddpma_status issue(ddpma_plan* p, std::vector<Entry>& ents, int slot) {
+  const int n = (int)p->local.size();
+  const int nb = prefix_tiles(p, ents);
+  memcpy(p->h_ent[slot], ents.data(), sizeof(Entry) * ents.size());
+  SubRes* res = p->d_ring + (size_t)slot * n;
+  double* part = p->d_partring + (size_t)slot * std::max(p->total_tiles, 1);
+  CK(p, cudaMemsetAsync(res, 0, sizeof(SubRes) * n, p->st));
+  CK(p, cudaMemcpyAsync(p->d_ent[slot], p->h_ent[slot], sizeof(Entry) * ents.size(),
+                        cudaMemcpyHostToDevice, p->st));
   KArgs a = base_args(p);
-  a.ent = d_ents;
-  a.nent = nent;
-  a.j = j;
-  a.coef = d_coef;
+  a.ent = p->d_ent[slot];
+  a.nent = (int)ents.size();
+  a.res = res;
+  a.part = part;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->prof) {
     e0 = take_event(p);
     e1 = take_event(p);
     cudaEventRecord(e0, p->st);
   }
-  launch_eval(mode, a, nblocks, p->st);
-  const long long nodes = entries_nodes(p, h_ents, nent);
+  launch_eval(a, nb, p->st);
+  double bytes = 0.0;
+  long long nodes = 0;
+  bool sums = false;
+  for (auto& e : ents) {
+    const long long nn = p->geo[e.sub].nodes;
+    bytes += mode_bytes(e.mode) * (double)nn;
+    p->mode_nodes[e.mode] += nn;
+    if (e.mode != M_NORM) {
+      nodes += nn;
+      p->rhs_evals += 1;
+    }
+    sums |= e.mode == M_POWER || e.mode == M_POWER_SEED || e.mode == M_NORM;
+  }
   if (p->prof) {
     cudaEventRecord(e1, p->st);
-    p->prof_pending.push_back({e0, e1, klass, bpn * (double)nodes, nodes});
+    p->prof_pending.push_back({e0, e1, 0, bytes, nodes});
   }
-  account(p, klass, nodes, bpn, true);
-  p->rhs_evals += nent;
+  p->launches += 1;
+  p->algo_bytes += bytes;
+  p->node_updates += nodes;
+  p->prof_launches[0] += 1;
+  p->prof_bytes[0] += bytes;
+  p->prof_nodes[0] += nodes;
+  if (sums) launch_finalize(p->d_ent[slot], (int)ents.size(), part, res, 0, p->st);
+  CK(p, cudaMemcpyAsync(p->h_ring + (size_t)slot * n, res, sizeof(SubRes) * n,
+                        cudaMemcpyDeviceToHost, p->st));
+  CK(p, cudaEventRecord(p->ring_ev[slot], p->st));
   return check_launch(p, "eval kernel");
+}
+
+// Synchronous single launch (operator-level exports): results in h_ring slot 0.
+ddpma_status issue_sync(ddpma_plan* p, std::vector<Entry>& ents) {
+  ddpma_status s = issue(p, ents, 0);
+  if (s != DDPMA_OK) return s;
+  return sync(p);
 }
 
 void prof_collect(ddpma_plan* p) {
@@ -432,10 +525,11 @@ void begin_window_ctl(ddpma_plan* p, int l) {
   }
 }
 
-void on_result(ddpma_plan* p, int l, Phase ph) {
+// Decision after an action's result (integrate.py:180-250 restated).
+void on_result(ddpma_plan* p, int l, Phase ph, const SubRes& r) {
   Ctl& c = p->ctl[l];
-  const SubRes& r = p->h_res[l];
   const double total = p->cfg.dtau;
+  c.waiting = false;
   switch (ph) {
     case PH_F0:
       c.start_flag = (r.flags & 1u) != 0;
@@ -474,11 +568,12 @@ void on_result(ddpma_plan* p, int l, Phase ph) {
     }
     case PH_STEP: {                             // integrate.py:203-249
       const bool nonfin = (r.flags & 4u) != 0;
-      const bool flagged = (r.flags & 3u) != 0;
+      const bool flagged = c.step_flag || (r.flags & 3u) != 0;
       const bool end_flag = (r.flags & 2u) != 0;
       const double emax = bits_dec(r.emax);
       const bool flag_fail = flagged && !c.state_flag && c.flag_rej < 8;
       const bool bad = flag_fail || nonfin;
+      c.j_next = 0;
       if (g_trace)
         fprintf(stderr, "TRACE %d step %.17g %d %.17g %d %d\n", p->local[l], c.h, c.s,
                 nonfin ? NAN : emax, flagged ? 1 : 0, (!bad && emax <= 1.0) ? 1 : 0);
@@ -519,159 +614,252 @@ void on_result(ddpma_plan* p, int l, Phase ph) {
       }
       break;
     }
-    case PH_EULER:
-      c.yi ^= 1;
-      if (--c.euler_left == 0) c.phase = PH_DONE;
-      break;
     default:
       break;
   }
 }
 
-// One window of integration for the local subdomains `act` (local indices).
-ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
-  for (int l : act) begin_window_ctl(p, l);
-  std::vector<Phase> phase_of(p->local.size(), PH_IDLE);
-  while (true) {
-    std::vector<int> f0s, norms, pows_seed, pows, steps, eulers;
-    for (int l : act) {
-      switch (p->ctl[l].phase) {
-        case PH_F0: f0s.push_back(l); break;
-        case PH_SIG_NORM: norms.push_back(l); break;
-        case PH_SIG_ITER: (p->ctl[l].vin < 0 ? pows_seed : pows).push_back(l); break;
-        case PH_STEP: steps.push_back(l); break;
-        case PH_EULER: eulers.push_back(l); break;
-        default: break;
-      }
-      phase_of[l] = p->ctl[l].phase;
-    }
-    if (f0s.empty() && norms.empty() && pows_seed.empty() && pows.empty() && steps.empty() &&
-        eulers.empty())
+// The next action of subdomain l as a launch entry; updates the host-side
+// bookkeeping of actions that need no decision (stages, Euler substeps).
+Entry next_action(ddpma_plan* p, int l) {
+  Ctl& c = p->ctl[l];
+  Entry e = make_entry(p, l);
+  switch (c.phase) {
+    case PH_F0:
+      e.mode = M_F0;
+      c.waiting = true;
       break;
-    launch_res_init(p->d_res, (int)p->local.size(), p->st);
-    ddpma_status s;
-    if (!f0s.empty()) {            // f0 = F(y) (integrate.py:184)
-      std::vector<Entry> ents;
-      for (int l : f0s) ents.push_back(make_entry(p, l));
-      const int nb = prefix_tiles(p, ents);
-      void* d;
-      if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &d)) != DDPMA_OK) return s;
-      if ((s = eval_launch(p, M_F0, (Entry*)d, ents.data(), (int)ents.size(), nb, 0, nullptr, 3,
-                           24.0)) != DDPMA_OK)
-        return s;
-    }
-    if (!norms.empty()) {          // ||y|| (integrate.py:133)
-      std::vector<Entry> ents;
-      for (int l : norms) ents.push_back(make_entry(p, l));
-      const int nb = prefix_tiles(p, ents);
-      void* d;
-      if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &d)) != DDPMA_OK) return s;
-      KArgs a = base_args(p);
-      a.ent = (Entry*)d;
-      a.nent = (int)ents.size();
-      launch_sumsq(a, nb, p->st);
-      launch_finalize((Entry*)d, (int)ents.size(), p->d_part, p->d_res, 0, p->st);
-      account(p, 6, entries_nodes(p, ents.data(), (int)ents.size()), 8.0, false);
-      if ((s = check_launch(p, "sumsq")) != DDPMA_OK) return s;
-    }
-    for (int pass = 0; pass < 2; ++pass) {   // power iteration (integrate.py:135-141)
-      const std::vector<int>& grp = pass == 0 ? pows_seed : pows;
-      if (grp.empty()) continue;
-      std::vector<Entry> ents;
-      for (int l : grp) {
-        Entry e = make_entry(p, l);
-        Ctl& c = p->ctl[l];
-        e.vin = c.vin;
-        c.vout = c.vin < 0 ? 0 : 1 - c.vin;
-        e.vout = c.vout;
-        e.c = c.delta / c.vnorm;
-        ents.push_back(e);
+    case PH_SIG_NORM:
+      e.mode = M_NORM;
+      c.waiting = true;
+      break;
+    case PH_SIG_ITER:
+      e.mode = c.vin < 0 ? M_POWER_SEED : M_POWER;
+      e.vin = c.vin;
+      c.vout = c.vin < 0 ? 0 : 1 - c.vin;
+      e.vout = c.vout;
+      e.c = c.delta / c.vnorm;
+      c.waiting = true;
+      break;
+    case PH_STEP: {
+      const RkcCoeffs& rc = coeffs(p, c.s);
+      if (c.j_next == 0) {
+        c.j_next = 2;
+        c.step_flag = false;
       }
-      const int nb = prefix_tiles(p, ents);
-      void* d;
-      if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &d)) != DDPMA_OK) return s;
-      if ((s = eval_launch(p, pass == 0 ? M_POWER_SEED : M_POWER, (Entry*)d, ents.data(),
-                           (int)ents.size(), nb, 0, nullptr, 4, pass == 0 ? 32.0 : 40.0)) !=
-          DDPMA_OK)
-        return s;
-      launch_finalize((Entry*)d, (int)ents.size(), p->d_part, p->d_res, 0, p->st);
-      // part is reused by the next group: the finalize above is stream-ordered before it
-    }
-    if (!steps.empty()) {          // _rkc_step (integrate.py:163-178)
-      std::sort(steps.begin(), steps.end(), [&](int x, int y) {
-        if (p->ctl[x].s != p->ctl[y].s) return p->ctl[x].s > p->ctl[y].s;
-        return x < y;
-      });
-      std::vector<Entry> ents;
-      std::vector<Coef> coefs;
-      for (int l : steps) {
-        Ctl& c = p->ctl[l];
-        RkcCoeffs rc;
-        rkc_coeffs(c.s, rc);
-        Entry e = make_entry(p, l);
-        e.s = c.s;
-        e.coef = (int)coefs.size();
-        e.c = c.h * rc.mu1t;
+      e.s = c.s;
+      e.c = c.h * rc.mu1t;
+      if (c.j_next <= c.s) {
+        const int j = c.j_next++;
+        e.mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
+        e.j = j;
+        e.mu = rc.mu[j];
+        e.nu = rc.nu[j];
+        e.hmut = c.h * rc.mut[j];
+        e.hgt = c.h * rc.gt[j];
+      } else {
+        e.mode = M_FINAL;
         e.h04 = 0.4 * c.h;
-        for (int j = 0; j <= c.s; ++j) {
-          Coef q{};
-          if (j >= 2) {
-            q.mu = rc.mu[j];
-            q.nu = rc.nu[j];
-            q.hmut = c.h * rc.mut[j];
-            q.hgt = c.h * rc.gt[j];
-          }
-          coefs.push_back(q);
-        }
-        ents.push_back(e);
+        c.waiting = true;
       }
-      const int total_nb = prefix_tiles(p, ents);
-      void *de, *dc;
-      if ((s = stage_reserve(p, round_up(ents.size() * sizeof(Entry), 256) +
-                                    round_up(coefs.size() * sizeof(Coef), 256))) != DDPMA_OK)
-        return s;
-      if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &de)) != DDPMA_OK) return s;
-      if ((s = stage_put(p, coefs.data(), coefs.size() * sizeof(Coef), &dc)) != DDPMA_OK) return s;
-      const int smax = ents[0].s;
-      int m = (int)ents.size();
-      for (int j = 2; j <= smax; ++j) {
-        while (m > 0 && ents[m - 1].s < j) --m;
-        const int nb = m < (int)ents.size() ? ents[m].tile_begin : total_nb;
-        const int mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
-        const int klass = j >= 4 ? 0 : 1;
-        const double bpn = j == 2 ? 32.0 : (j == 3 ? 40.0 : 48.0);
-        if ((s = eval_launch(p, mode, (Entry*)de, ents.data(), m, nb, j, (Coef*)dc, klass, bpn)) !=
-            DDPMA_OK)
-          return s;
-      }
-      if ((s = eval_launch(p, M_FINAL, (Entry*)de, ents.data(), (int)ents.size(), total_nb, 0,
-                           (Coef*)dc, 2, 48.0)) != DDPMA_OK)
-        return s;
+      break;
     }
-    if (!eulers.empty()) {         // EulerIntegrator (integrate.py:69-74)
-      std::vector<Entry> ents;
-      for (int l : eulers) {
-        Entry e = make_entry(p, l);
-        e.c = p->cfg.dtau / (double)p->cfg.substeps;
-        ents.push_back(e);
-      }
-      const int nb = prefix_tiles(p, ents);
-      void* d;
-      if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &d)) != DDPMA_OK) return s;
-      if ((s = eval_launch(p, M_EULER, (Entry*)d, ents.data(), (int)ents.size(), nb, 0, nullptr,
-                           3, 24.0)) != DDPMA_OK)
-        return s;
-    }
-    CK(p, cudaMemcpyAsync(p->h_res, p->d_res, sizeof(SubRes) * p->local.size(),
-                          cudaMemcpyDeviceToHost, p->st));
-    if ((s = sync(p)) != DDPMA_OK) return s;
-    for (int l : act) {
-      const Phase ph = phase_of[l];
-      if (ph == PH_F0 || ph == PH_SIG_NORM || ph == PH_SIG_ITER || ph == PH_STEP || ph == PH_EULER)
-        on_result(p, l, ph);
+    case PH_EULER:
+      e.mode = M_EULER;
+      e.c = p->cfg.dtau / (double)p->cfg.substeps;
+      c.yi ^= 1;
+      if (--c.euler_left == 0) c.phase = PH_DONE;
+      break;
+    default:
+      e.mode = -1;
+      break;
+  }
+  return e;
+}
+
+struct Inflight {
+  int slot;
+  std::vector<std::pair<int, int>> who;   // (local sub, mode)
+  std::vector<Phase> phase;                // phase at issue
+};
+
+// Process one completed launch: accumulate stage flags, run decisions.
+ddpma_status process(ddpma_plan* p, const Inflight& f) {
+  CK(p, cudaEventSynchronize(p->ring_ev[f.slot]));
+  const int n = (int)p->local.size();
+  const SubRes* res = p->h_ring + (size_t)f.slot * n;
+  for (size_t i = 0; i < f.who.size(); ++i) {
+    const int l = f.who[i].first, mode = f.who[i].second;
+    Ctl& c = p->ctl[l];
+    if (c.phase == PH_FAILED) continue;
+    const SubRes& r = res[l];
+    if (mode == M_STAGE2 || mode == M_STAGE3 || mode == M_STAGEN) {
+      c.step_flag = c.step_flag || (r.flags & 1u) != 0;
+    } else if (mode == M_EULER) {
+      // no decision (EulerIntegrator ignores the flag, integrate.py:72)
+    } else {
+      on_result(p, l, f.phase[i], r);
     }
   }
   return DDPMA_OK;
+}
+
+// One window of integration for the local subdomains `act`: an asynchronous
+// pipeline.  Every launch carries one action for each subdomain that is not
+// waiting on a host decision (stages of different steps, power iterations,
+// f0 evaluations mix freely); the result of launch k is processed while
+// launch k+1 runs, so a decision costs a subdomain one skipped launch.
+ddpma_status advance_set_host(ddpma_plan* p, const std::vector<int>& act) {
+  for (int l : act) {
+    begin_window_ctl(p, l);
+    p->ctl[l].waiting = false;
+    p->ctl[l].j_next = 0;
+  }
+  std::vector<Inflight> q;   // FIFO (front = oldest)
+  size_t head = 0;
+  ddpma_status s;
+  while (true) {
+    std::vector<Entry> ents;
+    Inflight f;
+    for (int l : act) {
+      Ctl& c = p->ctl[l];
+      if (c.waiting) continue;
+      if (c.phase != PH_F0 && c.phase != PH_SIG_NORM && c.phase != PH_SIG_ITER &&
+          c.phase != PH_STEP && c.phase != PH_EULER)
+        continue;
+      const Phase ph = c.phase;
+      Entry e = next_action(p, l);
+      f.who.push_back({l, e.mode});
+      f.phase.push_back(ph);
+      ents.push_back(e);
+    }
+    if (!ents.empty()) {
+      f.slot = (int)(p->kissue % ddpma_plan::R);
+      if ((s = issue(p, ents, f.slot)) != DDPMA_OK) return s;
+      p->kissue++;
+      q.push_back(std::move(f));
+    }
+    const size_t inflight = q.size() - head;
+    if (inflight == 0) break;
+    if (ents.empty() || inflight >= 2) {
+      if ((s = process(p, q[head])) != DDPMA_OK) return s;
+      ++head;
+    }
+  }
+  return sync(p);
+}
+
+// One window on the device-resident controller: window-begin kernel + one
+// cooperative persistent kernel (persist.cu), then one read-back of the
+// controller states.  This is the production path.
+ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
+  if (p->host_ctl) return advance_set_host(p, act);
+  const int nl = (int)p->local.size();
+  // priority: most RHS evaluations in the previous window first (the
+  // straggler's critical path is served before filler work)
+  std::vector<int> order(act);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return p->last_evals[x] * p->geo[x].nodes > p->last_evals[y] * p->geo[y].nodes;
+  });
+  for (size_t q = 0; q < order.size(); ++q) p->h_act[q] = order[q];
+  CK(p, cudaMemcpyAsync(p->d_act, p->h_act, sizeof(int) * act.size(), cudaMemcpyHostToDevice, p->st));
+  CK(p, cudaMemsetAsync(p->d_ndone, 0, sizeof(unsigned int) * 2, p->st));
+  WinArgs A{};
+  A.P = p->P;
+  A.geo = p->d_geo;
+  A.F = p->F;
+  A.ctl = p->d_ctl;
+  A.act = p->d_act;
+  A.nact = (int)act.size();
+  A.scheme = p->cfg.scheme;
+  A.substeps = p->cfg.substeps;
+  A.max_stages = p->cfg.max_stages;
+  A.dtau = p->cfg.dtau;
+  A.coef = p->d_coef;
+  A.coef_off = p->d_coef_off;
+  A.part = p->d_part_items;
+  A.poff = p->d_poff;
+  A.n_done = p->d_ndone;
+  A.trace = p->d_trace;
+  A.trace_n = p->d_trace_n;
+  A.trace_cap = p->trace_cap;
+  launch_window_begin(A, p->st);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (p->prof) {
+    e0 = take_event(p);
+    e1 = take_event(p);
+    cudaEventRecord(e0, p->st);
+  }
+  launch_window(A, p->win_blocks, p->st);
+  if (p->prof) cudaEventRecord(e1, p->st);
+  ddpma_status s = check_launch(p, "window kernel");
+  if (s != DDPMA_OK) return s;
+  CK(p, cudaMemcpyAsync(p->h_ctl, p->d_ctl, sizeof(DevCtl) * nl, cudaMemcpyDeviceToHost, p->st));
+  unsigned int ntr = 0;
+  if (p->d_trace) CK(p, cudaMemcpyAsync(&ntr, p->d_trace_n, sizeof(unsigned), cudaMemcpyDeviceToHost, p->st));
+  CK(p, cudaStreamSynchronize(p->st));
+  double bytes = 0.0;
+  long long nodes = 0;
+  for (int l : act) {
+    const DevCtl& c = p->h_ctl[l];
+    DevCtl& prev = p->ctl_prev[l];
+    const long long de = c.evals - prev.evals;
+    p->last_evals[l] = de;
+    bytes += c.bytes - prev.bytes;
+    nodes += de * p->geo[l].nodes;
+    p->rhs_evals += de;
+    prev.evals = c.evals;
+    prev.bytes = c.bytes;
+    p->ctl[l].yi = c.yi;
+    p->ctl[l].fi = c.fi;
+    if (c.fail_status != 0) {
+      const int gid = p->local[l];
+      if (!p->fail.set || gid < p->fail.gid) {
+        p->fail = Failure{};
+        p->fail.set = true;
+        p->fail.gid = gid;
+        p->fail.status = (ddpma_status)c.fail_status;
+        p->fail.msg = c.fail_status == DDPMA_ERR_VALUE ? "cannot convert float NaN to integer"
+                      : c.fail_status == DDPMA_ERR_OVERFLOW ? "cannot convert float infinity to integer"
+                                                            : "internal step underflow";
+        p->fail.t = c.fail_t;
+        p->fail.h = c.fail_h;
+        p->fail.local = l;
+        p->fail.s = c.fail_s;
+        p->fail.yi = c.fail_yi;
+        p->fail.fi = c.fail_fi;
+        p->fail.h04 = c.fail_h04;
+        p->fail.nnodes = c.fail_nonfin ? -1 : -2;
+      }
+    }
+  }
+  if (getenv("DDPMA_TIMELINE")) {
+    unsigned long long t0 = ~0ull;
+    for (int l : act) t0 = std::min(t0, p->h_ctl[l].t_begin);
+    fprintf(stderr, "TIMELINE");
+    for (int l : act)
+      fprintf(stderr, " %d:%.2fms/%lld", p->local[l], (p->h_ctl[l].t_done - t0) * 1e-6,
+              p->h_ctl[l].evals);
+    fprintf(stderr, "\n");
+  }
+  p->node_updates += nodes;
+  p->algo_bytes += bytes;
+  p->launches += 2;
+  p->prof_launches[0] += 1;
+  p->prof_bytes[0] += bytes;
+  p->prof_nodes[0] += nodes;
+  if (p->prof) p->prof_pending.push_back({e0, e1, 0, 0.0, 0});
+  if (ntr > 0 && p->d_trace) {
+    std::vector<TraceRec> tr(std::min<unsigned>(ntr, (unsigned)p->trace_cap));
+    CK(p, cudaMemcpy(tr.data(), p->d_trace, sizeof(TraceRec) * tr.size(), cudaMemcpyDeviceToHost));
+    for (auto& r : tr) {
+      if (r.kind == 1) fprintf(stderr, "TRACE %d sigma %.17g\n", r.sub, r.val);
+      else
+        fprintf(stderr, "TRACE %d step %.17g %d %.17g %d %d\n", r.sub, r.h, r.s, r.val, r.flagged,
+                r.accepted);
+    }
+  }
+  return sync(p);
 }
 
 // Entries for every local subdomain (current buffers).
@@ -959,6 +1147,24 @@ extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   cudaFree(p->d_stage);
   cudaFree(p->d_scratch);
   if (p->h_res) cudaFreeHost(p->h_res);
+  for (int r = 0; r < ddpma_plan::R; ++r) {
+    if (p->h_ent[r]) cudaFreeHost(p->h_ent[r]);
+    cudaFree(p->d_ent[r]);
+    if (p->ring_ev[r]) cudaEventDestroy(p->ring_ev[r]);
+  }
+  cudaFree(p->d_ring);
+  if (p->h_ring) cudaFreeHost(p->h_ring);
+  cudaFree(p->d_partring);
+  cudaFree(p->d_ctl);
+  if (p->h_ctl) cudaFreeHost(p->h_ctl);
+  cudaFree(p->d_coef);
+  cudaFree(p->d_coef_off);
+  cudaFree(p->d_part_items);
+  cudaFree(p->d_poff);
+  cudaFree(p->d_act);
+  if (p->h_act) cudaFreeHost(p->h_act);
+  cudaFree(p->d_ndone);
+  cudaFree(p->d_trace);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->st) cudaStreamDestroy(p->st);
   delete p;
@@ -1118,6 +1324,16 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
       g.tiles_z = g.n[0];
     }
     g.ntiles = g.tiles_x * g.tiles_y * g.tiles_z;
+    if (p->dim == 2) {
+      g.items_x = (g.n[1] + TX - 1) / TX;
+      g.items_y = (g.n[0] + IR2 - 1) / IR2;
+      g.items_z = 1;
+    } else {
+      g.items_x = (g.n[2] + TX - 1) / TX;
+      g.items_y = (g.n[1] + TY - 1) / TY;
+      g.items_z = (g.n[0] + IZ3 - 1) / IZ3;
+    }
+    g.nitems = g.items_x * g.items_y * g.items_z;
     tiles += g.ntiles;
     p->geo.push_back(g);
   }
@@ -1162,6 +1378,74 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     return fail(ce, "part");
   if ((ce = cudaMalloc((void**)&p->d_part2, sizeof(double) * std::max(tiles, 1))) != cudaSuccess)
     return fail(ce, "part2");
+  for (int r = 0; r < ddpma_plan::R; ++r) {
+    if ((ce = cudaMallocHost((void**)&p->h_ent[r], sizeof(Entry) * p->local.size())) != cudaSuccess)
+      return fail(ce, "ent host");
+    if ((ce = cudaMalloc((void**)&p->d_ent[r], sizeof(Entry) * p->local.size())) != cudaSuccess)
+      return fail(ce, "ent dev");
+    if ((ce = cudaEventCreateWithFlags(&p->ring_ev[r], cudaEventDisableTiming)) != cudaSuccess)
+      return fail(ce, "ring event");
+  }
+  if ((ce = cudaMalloc((void**)&p->d_ring, sizeof(SubRes) * p->local.size() * ddpma_plan::R)) !=
+      cudaSuccess)
+    return fail(ce, "ring");
+  if ((ce = cudaMallocHost((void**)&p->h_ring, sizeof(SubRes) * p->local.size() * ddpma_plan::R)) !=
+      cudaSuccess)
+    return fail(ce, "ring host");
+  if ((ce = cudaMalloc((void**)&p->d_partring,
+                       sizeof(double) * std::max(tiles, 1) * ddpma_plan::R)) != cudaSuccess)
+    return fail(ce, "part ring");
+  {   // device controller: state, RKC2 tables, item partials, trace
+    const int nl = (int)p->local.size();
+    if ((ce = cudaMalloc((void**)&p->d_ctl, sizeof(DevCtl) * nl)) != cudaSuccess) return fail(ce, "ctl");
+    if ((ce = cudaMallocHost((void**)&p->h_ctl, sizeof(DevCtl) * nl)) != cudaSuccess) return fail(ce, "ctl host");
+    memset(p->h_ctl, 0, sizeof(DevCtl) * nl);
+    const int ms = std::max(2, cfg->max_stages);
+    std::vector<int> off(ms + 1, 0);
+    std::vector<double> tab;
+    for (int sst = 2; sst <= ms && cfg->scheme == DDPMA_SCHEME_ADAPTIVE; ++sst) {
+      off[sst] = (int)(tab.size() / 4);
+      const RkcCoeffs& rc = coeffs(p, sst);
+      for (int j = 0; j <= sst; ++j) {
+        if (j == 0) {
+          tab.insert(tab.end(), {rc.mu1t, rc.w0, rc.w1, 0.0});
+        } else {
+          tab.insert(tab.end(), {rc.mu[j], rc.nu[j], rc.mut[j], rc.gt[j]});
+        }
+      }
+    }
+    p->coeff_cache.clear();
+    p->coeff_cache.shrink_to_fit();
+    if (tab.empty()) tab.assign(4, 0.0);
+    if ((ce = cudaMalloc((void**)&p->d_coef, sizeof(double) * tab.size())) != cudaSuccess) return fail(ce, "coef");
+    if ((ce = cudaMemcpy(p->d_coef, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(ce, "coef copy");
+    if ((ce = cudaMalloc((void**)&p->d_coef_off, sizeof(int) * off.size())) != cudaSuccess) return fail(ce, "coef off");
+    if ((ce = cudaMemcpy(p->d_coef_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(ce, "coef off copy");
+    std::vector<long long> poff(nl);
+    long long acc = 0;
+    for (int l = 0; l < nl; ++l) {
+      poff[l] = acc;
+      acc += p->geo[l].nitems;
+    }
+    if ((ce = cudaMalloc((void**)&p->d_part_items, sizeof(double) * std::max(acc, 1LL))) != cudaSuccess)
+      return fail(ce, "part items");
+    if ((ce = cudaMalloc((void**)&p->d_poff, sizeof(long long) * nl)) != cudaSuccess) return fail(ce, "poff");
+    if ((ce = cudaMemcpy(p->d_poff, poff.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(ce, "poff copy");
+    if ((ce = cudaMalloc((void**)&p->d_act, sizeof(int) * nl)) != cudaSuccess) return fail(ce, "act");
+    if ((ce = cudaMallocHost((void**)&p->h_act, sizeof(int) * nl)) != cudaSuccess) return fail(ce, "act host");
+    if ((ce = cudaMalloc((void**)&p->d_ndone, sizeof(unsigned int) * 2)) != cudaSuccess) return fail(ce, "ndone");
+    p->d_trace_n = p->d_ndone + 1;
+    if (g_trace) {
+      p->trace_cap = 1 << 22;
+      if ((ce = cudaMalloc((void**)&p->d_trace, sizeof(TraceRec) * p->trace_cap)) != cudaSuccess)
+        return fail(ce, "trace");
+    }
+    p->win_blocks = window_blocks(p->dim, P.pow2);
+    p->host_ctl = getenv("DDPMA_HOST_CONTROLLER") != nullptr;
+  }
   p->stage_cap = 1 << 20;
   if ((ce = cudaMallocHost((void**)&p->h_stage, p->stage_cap)) != cudaSuccess) return fail(ce, "stage");
   if ((ce = cudaMalloc((void**)&p->d_stage, p->stage_cap)) != cudaSuccess) return fail(ce, "stage dev");
@@ -1174,6 +1458,14 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
 extern "C" ddpma_status ddpma_set_state(ddpma_plan* p, const double* psi_global_host) {
   CK(p, cudaSetDevice(p->device));
   for (auto& c : p->ctl) c = Ctl{};   // fresh integrators (schwarz.py:133)
+  {
+    const int nl = (int)p->local.size();
+    memset(p->h_ctl, 0, sizeof(DevCtl) * nl);
+    for (int l = 0; l < nl; ++l) p->h_ctl[l].interval = 25;   // _SIGMA_REFRESH
+    CK(p, cudaMemcpyAsync(p->d_ctl, p->h_ctl, sizeof(DevCtl) * nl, cudaMemcpyHostToDevice, p->st));
+    p->ctl_prev.assign(nl, DevCtl{});
+    p->last_evals.assign(nl, 0);
+  }
   int nb;
   std::vector<Entry> ents = all_entries(p, &nb);
   void* d;
@@ -1603,18 +1895,10 @@ extern "C" ddpma_status ddpma_rhs_frozen(ddpma_plan* p, int sub_id, const double
   set_guard(p, rho_max);
   std::vector<int> one{l};
   if ((s = prologue(p, one, 1.0)) != DDPMA_OK) return s;   // mr = measure*(rho/1.0)
-  launch_res_init(p->d_res, (int)p->local.size(), p->st);
-  void* d;
-  int nb;
   std::vector<Entry> ents{make_entry(p, l)};
-  nb = prefix_tiles(p, ents);
-  if ((s = stage_put(p, ents.data(), sizeof(Entry), &d)) != DDPMA_OK) return s;
-  if ((s = eval_launch(p, M_F0, (Entry*)d, ents.data(), 1, nb, 0, nullptr, 3, 24.0)) != DDPMA_OK)
-    return s;
-  CK(p, cudaMemcpyAsync(p->h_res, p->d_res, sizeof(SubRes) * p->local.size(),
-                        cudaMemcpyDeviceToHost, p->st));
-  if ((s = sync(p)) != DDPMA_OK) return s;
-  *flag = (p->h_res[l].flags & 1u) ? 1 : 0;
+  ents[0].mode = M_F0;
+  if ((s = issue_sync(p, ents)) != DDPMA_OK) return s;
+  *flag = (p->h_ring[l].flags & 1u) ? 1 : 0;
   return d2h_box(p, l, p->F.f[0], F_out);
 }
 
@@ -1730,35 +2014,29 @@ extern "C" ddpma_status ddpma_rkc_step(ddpma_plan* p, int sub_id, const double* 
   c.fi = 0;
   c.h = h;
   c.s = s_stages;
-  RkcCoeffs rc;
-  rkc_coeffs(s_stages, rc);
-  Entry e = make_entry(p, l);
-  e.s = s_stages;
-  e.coef = 0;
-  e.c = h * rc.mu1t;
-  e.h04 = 0.4 * h;
-  std::vector<Entry> ents{e};
-  const int nb = prefix_tiles(p, ents);
-  std::vector<Coef> coefs(s_stages + 1);
-  for (int j = 2; j <= s_stages; ++j) coefs[j] = Coef{rc.mu[j], rc.nu[j], h * rc.mut[j], h * rc.gt[j]};
-  void *de, *dc;
-  if ((s = stage_reserve(p, 256 + round_up(coefs.size() * sizeof(Coef), 256))) != DDPMA_OK) return s;
-  if ((s = stage_put(p, ents.data(), sizeof(Entry), &de)) != DDPMA_OK) return s;
-  if ((s = stage_put(p, coefs.data(), coefs.size() * sizeof(Coef), &dc)) != DDPMA_OK) return s;
-  launch_res_init(p->d_res, (int)p->local.size(), p->st);
-  for (int j = 2; j <= s_stages; ++j) {
-    const int mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
-    if ((s = eval_launch(p, mode, (Entry*)de, ents.data(), 1, nb, j, (Coef*)dc, j >= 4 ? 0 : 1,
-                         48.0)) != DDPMA_OK)
-      return s;
+  const RkcCoeffs& rc = coeffs(p, s_stages);
+  bool stage_flag = false;
+  for (int j = 2; j <= s_stages + 1; ++j) {   // integrate.py:169-177, one launch per stage
+    Entry e = make_entry(p, l);
+    e.s = s_stages;
+    e.c = h * rc.mu1t;
+    e.h04 = 0.4 * h;
+    if (j <= s_stages) {
+      e.mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
+      e.j = j;
+      e.mu = rc.mu[j];
+      e.nu = rc.nu[j];
+      e.hmut = h * rc.mut[j];
+      e.hgt = h * rc.gt[j];
+    } else {
+      e.mode = M_FINAL;
+    }
+    std::vector<Entry> ents{e};
+    if ((s = issue_sync(p, ents)) != DDPMA_OK) return s;
+    if (j <= s_stages) stage_flag = stage_flag || (p->h_ring[l].flags & 1u);
   }
-  if ((s = eval_launch(p, M_FINAL, (Entry*)de, ents.data(), 1, nb, 0, (Coef*)dc, 2, 48.0)) != DDPMA_OK)
-    return s;
-  CK(p, cudaMemcpyAsync(p->h_res, p->d_res, sizeof(SubRes) * p->local.size(),
-                        cudaMemcpyDeviceToHost, p->st));
-  if ((s = sync(p)) != DDPMA_OK) return s;
-  *flagged = (p->h_res[l].flags & 3u) ? 1 : 0;
-  *end_flagged = (p->h_res[l].flags & 2u) ? 1 : 0;
+  *flagged = (stage_flag || (p->h_ring[l].flags & 3u)) ? 1 : 0;
+  *end_flagged = (p->h_ring[l].flags & 2u) ? 1 : 0;
   if ((s = d2h_box(p, l, p->F.d[s_stages % 3], d_out)) != DDPMA_OK) return s;
   return d2h_box(p, l, p->F.f[1], fnew_out);
 }

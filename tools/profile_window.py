@@ -1,0 +1,15 @@
+"""Run W warm-up windows of a BASELINE config, then one more window (the one
+ncu captures with -k regex:k_window -s W)."""
+import sys
+sys.path.insert(0, ".")
+import paper_2006_14602_b200 as P
+from paper_2006_14602_b200.plan import Plan
+import bench
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+W = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+g, d, m = bench.case(name, P)
+plan = Plan.for_grid(g, d.subdomains, m, P.SolverConfig(tol=1e-300, max_windows=W + 1, transmission="parallel"))
+plan.set_state(None)
+for w in range(W + 1):
+    plan.run(1, 1e-300)
+print("done", plan.counters())
