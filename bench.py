@@ -180,7 +180,8 @@ def cpu_sample(name, threads=None, target_s=12.0):
     geom, psi, rho, rmax = work[0]
     O.rhs_frozen(psi, rho, geom, O.DET_FLOOR, geom.mask(), rmax)
     t_eval = time.perf_counter() - one
-    s = int(max(2, min(64, target_s / max(t_eval * max(1, len(work) / cores), 1e-6))))
+    # the pool runs len(work) tasks of (s+1) evaluations on `cores` threads
+    s = int(max(2, min(512, target_s * cores / max(len(work) * t_eval, 1e-9) - 1)))
 
     def task(w):
         geom, psi, rho, rmax = w

@@ -289,10 +289,16 @@ ENVELOPE_RUNS = {
     "T3_parallel": ("T3", dict(max_windows=40, transmission="parallel"), None),
     "T3_alternating": ("T3", dict(max_windows=40, transmission="alternating"), None),
     "T3_single": ("T3s", dict(max_windows=40), None),
+    "C2_parallel_2": ("C2", dict(max_windows=2, transmission="parallel"), None),
+    "C4_parallel_1": ("C4", dict(max_windows=1, transmission="parallel"), None),
 }
 
 
 def _oracle_run(kind, kw, init):
+    if kind in ("C2", "C4"):
+        g, lay, ov, mon, _, _ = O.baseline_case(kind)
+        d = O.make_decomposition(g, lay, ov)
+        return O.solve(g, d, mon, g.extents, O.Config(tol=1e-300, **kw))
     if kind.startswith("T3"):
         g = O.make_grid(3, ((0, 1),) * 3, (33, 33, 33))
         mon, lay, ov = O.Shell(), (2, 2, 2), 4
