@@ -27,10 +27,10 @@ build/decomp.o: $(SRC)/decomp.cpp $(SRC)/ddpma_internal.h include/ddpma.h | buil
 build/plan.o: $(SRC)/plan.cu $(SRC)/ddpma_internal.h include/ddpma.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/plan.ptxas.log || (cat build/plan.ptxas.log; false)
 
-build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh | build
+build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(SRC)/fastlog.cuh $(SRC)/logtable.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/kernels.ptxas.log || (cat build/kernels.ptxas.log; false)
 
-build/persist.o: $(SRC)/persist.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh | build
+build/persist.o: $(SRC)/persist.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(SRC)/fastlog.cuh $(SRC)/logtable.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/persist.ptxas.log || (cat build/persist.ptxas.log; false)
 
 $(OUT): $(OBJ)

@@ -81,7 +81,7 @@ struct SubGeo {
   int items_x, items_y, items_z, nitems;   // persistent-kernel work items
 };
 
-constexpr int IR2 = 32;   // 2D work item: TX x IR2 nodes (each thread IR2/TY rows)
+constexpr int IR2 = 16;   // 2D work item: TX x IR2 nodes (each thread IR2/TY rows)
 constexpr int IZ3 = 8;    // 3D work item: TX x TY x IZ3 nodes
 
 // One participant (local subdomain) of a batched launch: its action (mode),
@@ -199,6 +199,9 @@ struct WinArgs {
   TraceRec* trace;
   unsigned int* trace_n;
   int trace_cap;
+  unsigned long long* probe;   // debug: [cap][4] = publish, first claim, last done, decided
+  int probe_sub, probe_cap;
+  int chunk_bulk;            // items per claim while >= 16 subdomains are active
 };
 
 void launch_window(const WinArgs& a, int nblocks, void* stream);

@@ -1,0 +1,78 @@
+// Table-driven natural logarithm for the hot kernel (host + device).
+//
+// CUDA's fp64 log() costs ~90 instructions per call and was 22% of the
+// window kernel's instruction stream (ncu, persist.cu).  This restates the
+// classic table method (Tang 1990; the same family numpy's AVX512 log uses):
+//   x = 2^e m, m in [0.75, 1.5);  k = rn(128 m), c = k/128, inv = rn(1/c)
+//   log x = e ln2 + T_k + log1p(r),  r = fma(m, inv, -1),  T_k = -log(inv)
+// with m*inv split exactly (r + plo), T_k in double-double (tools/gen_logtable.py), ln2 split so e*ln2_hi is
+// exact, and a degree-8 Taylor polynomial for log1p (|r| < 2^-7.5).  The
+// bucket of 1.0 has inv = 1, T = 0, so log(1) = 0 exactly and x near 1 keeps
+// full relative accuracy.  Max error measured by tools/test_fastlog.cpp (see its output in DESIGN.md).
+#pragma once
+
+#include <cmath>
+#include <cstring>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+#include "logtable.h"
+
+namespace ddpma {
+namespace dev {
+
+__host__ __device__ __forceinline__ double fastlog(double x) {
+#ifdef __CUDA_ARCH__
+  const double(*tab)[3] = kLogTabD;
+#define DDPMA_FMA(a, b, c) __fma_rn((a), (b), (c))
+#else
+  const double(*tab)[3] = kLogTabH;
+#define DDPMA_FMA(a, b, c) std::fma((a), (b), (c))
+#endif
+  if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
+  if (x == INFINITY) return x;
+  long long bits;
+  memcpy(&bits, &x, 8);
+  int e = (int)(bits >> 52) - 1023;
+  if (e == -1023) {   // subnormal: scale into the normal range
+    const double xs = x * 0x1p54;
+    memcpy(&bits, &xs, 8);
+    e = (int)(bits >> 52) - 1023 - 54;
+  }
+  const long long hb = (bits >> 51) & 1;   // m0 >= 1.5 -> m = m0/2
+  e += (int)hb;
+  const long long mb = (bits & 0x000FFFFFFFFFFFFFLL) | ((1023LL - hb) << 52);
+  double m;
+  memcpy(&m, &mb, 8);
+  const int k = (int)(m * 128.0 + 0.5);
+  const double* t = tab[k - 96];
+  const double pm = m * t[0];                   // m*inv = pm + plo exactly
+  const double plo = DDPMA_FMA(m, t[0], -pm);
+  const double r = pm - 1.0;                    // exact (Sterbenz: pm in [1-2^-7.5, 1+2^-7.5])
+  double q = -0.125;
+  q = DDPMA_FMA(q, r, 0x1.2492492492492p-3);    // 1/7
+  q = DDPMA_FMA(q, r, -0x1.5555555555555p-3);   // -1/6
+  q = DDPMA_FMA(q, r, 0.2);
+  q = DDPMA_FMA(q, r, -0.25);
+  q = DDPMA_FMA(q, r, 0x1.5555555555555p-2);    // 1/3
+  q = DDPMA_FMA(q, r, -0.5);
+  const double r2 = r * r;
+  const double ed = (double)e;
+  const double big = ed * kLn2Hi;               // exact
+  const double s = big + t[1];
+  const double err = (big - s) + t[1];          // Fast2Sum (|big| >= |T| or big = 0)
+  // log1p(r + plo) = log1p(r) + plo/(1+r) + O(plo^2): plo/(1+r) ~ plo - plo*r
+  const double lo = DDPMA_FMA(r2, q, (DDPMA_FMA(ed, kLn2Lo, t[2]) + err) + DDPMA_FMA(-plo, r, plo));
+  const double a = s + r;                       // TwoSum(s, r): r and T partially cancel near 1
+  const double bv = a - s;
+  const double e2 = (s - (a - bv)) + (r - bv);
+  return a + (e2 + lo);
+#undef DDPMA_FMA
+}
+
+}  // namespace dev
+}  // namespace ddpma

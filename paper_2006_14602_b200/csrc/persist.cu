@@ -828,6 +828,499 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A
   }
 }
 
+// ============================================================================
+// 2D window kernel with a chunked, double-buffered cp.async item pipeline.
+//
+// A CTA claims a CHUNK of consecutive work items of one subdomain action
+// (4 items while many subdomains are active, 1 on the tail's critical path),
+// then streams each item's sources into shared memory with 16-byte cp.async
+// (no register staging): the Y halo sources (y and the stage increment / f0 /
+// v tile, 34 x 36 each) and the centre fields the epilogue needs (|Omega|rho,
+// f0, d_{j-2}).  Item i+1's copies are in flight while item i is computed.
+// The arithmetic per node is exactly node()/hdet's (bitwise identical).
+// ============================================================================
+
+constexpr int TW2 = TX + 4;    // 36 doubles: columns c0-2 .. c0+33 (16-B aligned chunks)
+constexpr int TH2 = IR2 + 2;   // 34 rows
+struct Stage2 {
+  double ys[TH2 * TW2];
+  double as[TH2 * TW2];
+  double cm[IR2 * TX];
+  double cf[IR2 * TX];
+  double cd[IR2 * TX];
+};
+constexpr int STAGE2_BYTES = (int)sizeof(Stage2);
+
+__device__ __forceinline__ void cpa16(double* sdst, const double* gsrc, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int MODE, int YM>
+__device__ __forceinline__ void issue2(const WinArgs& A, const SubGeo& g, const Act& t, int item,
+                                       Stage2& st) {
+  const int ix = item % g.items_x, iy = item / g.items_x;
+  const int c0 = ix * TX, r0 = iy * IR2;
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  constexpr bool HAS_A = YM == YM_ADD || YM == YM_SCALED;
+  constexpr bool NEED_F0 = MODE == M_STAGE3 || MODE == M_STAGEN || MODE == M_FINAL ||
+                           MODE == M_POWER || MODE == M_POWER_SEED;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  constexpr int CH = TW2 / 2;   // 18 chunks per halo row
+  for (int e = tid; e < TH2 * CH; e += NT) {
+    const int rr = e / CH, cc = e - rr * CH;
+    const int i0 = r0 - 1 + rr, col = c0 - 2 + 2 * cc;
+    const bool ok = i0 >= 0 && i0 < g.n[0] && col >= 0 && col < g.pitch;
+    const long long k = ok ? g.off + (long long)i0 * g.pitch + col : g.off;
+    cpa16(&st.ys[rr * TW2 + 2 * cc], yb + k, ok ? 16 : 0);
+    if constexpr (HAS_A) cpa16(&st.as[rr * TW2 + 2 * cc], ap + k, ok ? 16 : 0);
+  }
+  if constexpr (MODE != M_NORM) {
+    constexpr int CC = TX / 2;  // 16 chunks per centre row
+    for (int e = tid; e < IR2 * CC; e += NT) {
+      const int rr = e / CC, cc = e - rr * CC;
+      const int i0 = r0 + rr, col = c0 + 2 * cc;
+      const bool ok = i0 < g.n[0] && col < g.pitch;
+      const long long k = ok ? g.off + (long long)i0 * g.pitch + col : g.off;
+      cpa16(&st.cm[rr * TX + 2 * cc], A.F.mr + k, ok ? 16 : 0);
+      if constexpr (NEED_F0) cpa16(&st.cf[rr * TX + 2 * cc], A.F.f[t.fi] + k, ok ? 16 : 0);
+      if constexpr (MODE == M_STAGEN)
+        cpa16(&st.cd[rr * TX + 2 * cc], A.F.d[(t.j - 2) % 3] + k, ok ? 16 : 0);
+    }
+  }
+  cpa_commit();
+}
+
+template <int YM>
+__device__ __forceinline__ double yat(const Stage2& st, int p, double c, int par) {
+  if constexpr (YM == YM_PLAIN) {
+    return st.ys[p];
+  } else if constexpr (YM == YM_ADD) {
+    return st.ys[p] + st.as[p];
+  } else if constexpr (YM == YM_SCALED) {
+    return st.ys[p] + c * st.as[p];
+  } else {
+    return st.ys[p] + (par ? -c : c);
+  }
+}
+
+// Y for the generic (box-face) formulas: from the smem tile when the point
+// lies inside it (always, except for 1-3 row/column slivers at a box end),
+// else from global memory.
+template <int YM, int YMG = YM>
+struct TileAcc2 {
+  const Stage2* st;
+  int r0, c0;
+  GAcc<2, YMG> g;
+  __device__ __forceinline__ double operator()(int i0, int i1, int) const {
+    const int rr = i0 - r0 + 1, cc = i1 - c0 + 2;
+    if (rr >= 0 && rr < TH2 && cc >= 0 && cc < TW2) {
+      const int p = rr * TW2 + cc;
+      if constexpr (YM == YM_PLAIN) {
+        return st->ys[p];
+      } else if constexpr (YM == YM_ADD) {
+        return st->ys[p] + st->as[p];
+      } else if constexpr (YM == YM_SCALED) {
+        return st->ys[p] + g.c * st->as[p];
+      } else {
+        return st->ys[p] + (((i0 + i1) & 1) ? -g.c : g.c);
+      }
+    }
+    return g(i0, i1, 0);
+  }
+};
+
+template <bool P2, int MODE, int YM>
+__device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int item,
+                                         const Stage2& st, Acc& acc, double* psum_item) {
+  constexpr int R = IR2 / TY;
+  // how Y is formed from global memory (outside the tile) for this mode
+  constexpr int YMG = MODE == M_STAGE2 ? YM_SCALED
+                      : (MODE == M_STAGE3 || MODE == M_STAGEN) ? YM_ADD : YM;
+  const int ix = item % g.items_x, iy = item / g.items_x;
+  const int c0 = ix * TX, r0 = iy * IR2;
+  const int n0 = g.n[0], n1 = g.n[1];
+  const int i1 = c0 + threadIdx.x;
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  if constexpr (MODE == M_NORM) {
+    double ps = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int lr = threadIdx.y + q * TY;
+      if (r0 + lr < n0 && i1 < n1) {
+        const double y = st.ys[(lr + 1) * TW2 + threadIdx.x + 2];
+        ps += y * y;
+      }
+    }
+    *psum_item = ps;
+    return;
+  } else {
+    // phase 1: determinants of all R rows, branch-free interior formula
+    // (independent chains -> ILP); box-face rows patched in phase 2
+    double det[R];
+    unsigned edge = 0u;   // bit q: node q is on a box face
+    unsigned valid = 0u;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int lr = threadIdx.y + q * TY;
+      const int i0 = r0 + lr;
+      const bool ok = i0 < n0 && i1 < n1;
+      valid |= ok ? (1u << q) : 0u;
+      const bool interior = i0 >= 1 && i0 <= n0 - 2 && i1 >= 1 && i1 <= n1 - 2;
+      edge |= (ok && !interior) ? (1u << q) : 0u;
+      const int p = (lr + 1) * TW2 + threadIdx.x + 2;
+      const int par = (i0 + i1) & 1;
+      const double yc = yat<YM>(st, p, t.c, par);
+      const double yn = yat<YM>(st, p - TW2, t.c, par ^ 1);
+      const double ys_ = yat<YM>(st, p + TW2, t.c, par ^ 1);
+      const double yw = yat<YM>(st, p - 1, t.c, par ^ 1);
+      const double ye = yat<YM>(st, p + 1, t.c, par ^ 1);
+      const double yne = yat<YM>(st, p - TW2 + 1, t.c, par);
+      const double ynw = yat<YM>(st, p - TW2 - 1, t.c, par);
+      const double yse = yat<YM>(st, p + TW2 + 1, t.c, par);
+      const double ysw = yat<YM>(st, p + TW2 - 1, t.c, par);
+      const double h00 = dv<P2>((ys_ - 2.0 * yc) + yn, A.P.ax[0].hh, A.P.ax[0].ihh);
+      const double h11 = dv<P2>((ye - 2.0 * yc) + yw, A.P.ax[1].hh, A.P.ax[1].ihh);
+      const double gp = dv<P2>(yse - ysw, A.P.ax[1].twoh, A.P.ax[1].itwoh);
+      const double gm = dv<P2>(yne - ynw, A.P.ax[1].twoh, A.P.ax[1].itwoh);
+      const double h01 = dv<P2>(gp - gm, A.P.ax[0].twoh, A.P.ax[0].itwoh);
+      det[q] = h00 * h11 - h01 * h01;
+    }
+    // phase 2: generic face formulas (rare)
+    if (edge) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (edge & (1u << q)) {
+          const int i0 = r0 + threadIdx.y + q * TY;
+          det[q] = hdet<2, P2>(A.P, g, i0, i1, 0,
+                               TileAcc2<YM, YMG>{&st, r0, c0, GAcc<2, YMG>{&g, yb, ap, t.c}});
+        }
+      }
+    }
+    // phase 3: log-equidistribution for all rows (independent chains)
+    double F[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int lr = threadIdx.y + q * TY;
+      const int i0 = r0 + lr;
+      const bool dir = ((edge >> q) & 1u) && dirichlet<2>(g, i0, i1, 0);   // faces only
+      const int pc = lr * TX + threadIdx.x;
+      F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor);
+      acc.flag |= ((valid >> q) & 1u) && det[q] <= A.P.floor && !dir ? 1u : 0u;
+    }
+    // phase 4: epilogues
+    double ps = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (!((valid >> q) & 1u)) continue;
+      const int lr = threadIdx.y + q * TY;
+      const int i0 = r0 + lr;
+      const int p = (lr + 1) * TW2 + threadIdx.x + 2;
+      const int pc = lr * TX + threadIdx.x;
+      const long long k = g.off + (long long)i0 * g.pitch + i1;
+      if constexpr (MODE == M_F0) {
+        A.F.f[t.fi][k] = F[q];
+      } else if constexpr (MODE == M_EULER) {
+        A.F.y[1 - t.yi][k] = st.ys[p] + t.c * F[q];
+      } else if constexpr (MODE == M_STAGE2) {
+        const double f0 = st.as[p];             // the a tile of stage 2 is f0
+        const double d1 = t.c * f0;
+        A.F.d[2][k] = ((t.mu * d1 + t.nu * 0.0) + t.hmut * F[q]) + t.hgt * f0;
+      } else if constexpr (MODE == M_STAGE3) {
+        const double f0 = st.cf[pc];
+        const double d1 = t.c * f0;
+        A.F.d[0][k] = ((t.mu * st.as[p] + t.nu * d1) + t.hmut * F[q]) + t.hgt * f0;
+      } else if constexpr (MODE == M_STAGEN) {
+        const double f0 = st.cf[pc];
+        A.F.d[t.j % 3][k] = ((t.mu * st.as[p] + t.nu * st.cd[pc]) + t.hmut * F[q]) + t.hgt * f0;
+      } else if constexpr (MODE == M_FINAL) {
+        const double ds = st.as[p], yv = st.ys[p], f0 = st.cf[pc];
+        const double yn = yv + ds;
+        A.F.f[1 - t.fi][k] = F[q];
+        A.F.y[1 - t.yi][k] = yn;
+        const double err = -0.8 * ds + t.h04 * (f0 + F[q]);
+        const double ay = fabs(yv), an = fabs(yn);
+        const double mx = (ay >= an || isnan(ay)) ? ay : an;
+        const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
+        if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
+        else acc.nonfin = 1;
+      } else {
+        const double diff = F[q] - st.cf[pc];
+        A.F.d[t.vout][k] = diff;
+        ps += diff * diff;
+      }
+    }
+    *psum_item = ps;
+  }
+}
+
+// Claim (warp 0): scan active subdomains in priority order, 32 at a time, and
+// grab up to `chunk` consecutive items of the first claimable action.
+__device__ __forceinline__ void claim(const WinArgs& A, int chunk, int& got, int& it0, int& nit) {
+  const int lane = threadIdx.x;
+  got = -1;
+  it0 = 0;
+  nit = 0;
+  for (int base = 0; base < A.nact && got < 0; base += 32) {
+    const int q = base + lane;
+    int l = -1;
+    bool claimable = false;
+    if (q < A.nact) {
+      l = A.act[q];
+      const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
+      claimable = (unsigned)(w & 0xffffffffull) < (unsigned)A.geo[l].nitems;
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, claimable);
+    while (mask != 0u && got < 0) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      int it = -1, n = 0;
+      if (lane == src) {
+        const unsigned long long w2 = atomicAdd(&A.ctl[l].word, (unsigned long long)chunk);
+        const unsigned u = (unsigned)(w2 & 0xffffffffull);
+        const unsigned ni = (unsigned)A.geo[l].nitems;
+        if (u < ni) {
+          it = (int)u;
+          n = (int)(ni - u < (unsigned)chunk ? ni - u : (unsigned)chunk);
+        }
+      }
+      it = __shfl_sync(0xffffffffu, it, src);
+      n = __shfl_sync(0xffffffffu, n, src);
+      if (it >= 0) {
+        got = __shfl_sync(0xffffffffu, l, src);
+        it0 = it;
+        nit = n;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ Act load_act(const WinArgs& A, int l) {
+  const DevCtl* gc = A.ctl + l;
+  Act t;
+  t.mode = __ldcg(&gc->a_mode);
+  t.j = __ldcg(&gc->a_j);
+  t.s = __ldcg(&gc->a_s);
+  t.yi = __ldcg(&gc->a_yi);
+  t.fi = __ldcg(&gc->a_fi);
+  t.vin = __ldcg(&gc->a_vin);
+  t.vout = __ldcg(&gc->a_vout);
+  t.sub = l;
+  t.c = __ldcg(&gc->a_c);
+  t.h04 = __ldcg(&gc->a_h04);
+  t.mu = __ldcg(&gc->a_mu);
+  t.nu = __ldcg(&gc->a_nu);
+  t.hmut = __ldcg(&gc->a_hmut);
+  t.hgt = __ldcg(&gc->a_hgt);
+  return t;
+}
+
+// Decision by warp 0 of the CTA that completed an action (see k_window).
+__device__ void decide(const WinArgs& A, int l, const SubGeo& g, double sum, DevCtl& s_ctl) {
+  DevCtl* gc = A.ctl + l;
+  constexpr int NW = (int)(sizeof(DevCtl) / 8);
+  constexpr int WI = (int)(offsetof(DevCtl, word) / 8);
+  long long* sc = reinterpret_cast<long long*>(&s_ctl);
+  const long long* gsrc = reinterpret_cast<const long long*>(gc);
+  for (int i = threadIdx.x; i < NW; i += 32) sc[i] = __ldcg(gsrc + i);
+  __syncwarp();
+  bool more = false;
+  unsigned long long seq = 0;
+  if (threadIdx.x == 0) {
+    d_complete(A, s_ctl, l, sum, g.nodes);
+    seq = (s_ctl.word >> 32) + 1;
+    more = d_next_action(A, s_ctl);
+    s_ctl.acc_flags = 0;
+    s_ctl.acc_emax = 0ull;
+    s_ctl.done = 0;
+    if (!more) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      s_ctl.t_done = now;
+    }
+  }
+  __syncwarp();
+  long long* gdst = reinterpret_cast<long long*>(gc);
+  for (int i = threadIdx.x; i < NW; i += 32)
+    if (i != WI) __stcg(gdst + i, sc[i]);
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (A.probe && l == A.probe_sub) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      const unsigned long long sq = (seq - 1) % (unsigned long long)A.probe_cap;
+      A.probe[sq * 4 + 3] = now;
+      A.probe[(seq % (unsigned long long)A.probe_cap) * 4 + 0] = now;
+    }
+    if (more) {
+      atomicExch(&gc->word, seq << 32);
+    } else {
+      atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+      atomicAdd(A.n_done, 1u);
+    }
+  }
+}
+
+template <bool P2, int MODE, int YM>
+__device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
+                       Stage2* stage, Acc& acc, double* sh_sum) {
+  constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
+  issue2<MODE, YM>(A, g, t, it0, stage[0]);
+  for (int i = 0; i < nit; ++i) {
+    if (i + 1 < nit) {
+      issue2<MODE, YM>(A, g, t, it0 + i + 1, stage[(i + 1) & 1]);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
+      // Y = y + d (or y + c*f0) once per tile point instead of 9x per node;
+      // the centre of the a tile (d_{j-1} / f0) stays intact for the epilogue
+      Stage2& sg = stage[i & 1];
+      const int tid = threadIdx.y * TX + threadIdx.x;
+      for (int e = tid; e < TH2 * TW2; e += NT) {
+        if constexpr (YM == YM_ADD) sg.ys[e] = sg.ys[e] + sg.as[e];
+        else sg.ys[e] = sg.ys[e] + t.c * sg.as[e];
+      }
+      __syncthreads();
+    }
+    double ps = 0.0;
+    constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
+    compute2<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, it0 + i, stage[i & 1], acc, &ps);
+    if constexpr (SUMS) {
+      const double s = block_sum(ps, sh_sum);   // per-item partial: deterministic
+      if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, s);
+    } else {
+      __syncthreads();   // the stage buffer is refilled by the next iteration's issue
+    }
+  }
+}
+
+template <bool P2>
+__device__ void dispatch_chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
+                                Stage2* st, Acc& acc, double* sh) {
+  switch (t.mode) {
+    case M_F0: chunk2<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_EULER: chunk2<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGE2: chunk2<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGE3: chunk2<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGEN: chunk2<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_FINAL: chunk2<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_POWER: chunk2<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_POWER_SEED: chunk2<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_NORM: chunk2<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    default: break;
+  }
+}
+
+template <bool P2>
+__global__ void __launch_bounds__(NT, 4) k_window2(const WinArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  Stage2* stage = reinterpret_cast<Stage2*>(dsm);
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_max[NT / 32];
+  __shared__ Act s_act;
+  __shared__ DevCtl s_ctl;
+  __shared__ int s_sub, s_it0, s_nit, s_exit, s_last;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  unsigned backoff = 32;
+  while (true) {
+    if (threadIdx.y == 0) {
+      // chunk of 4 items while many subdomains are active, 1 on the tail
+      const unsigned nd = *(volatile unsigned*)A.n_done;
+      const int chunk = (A.nact - (int)nd) >= 16 ? A.chunk_bulk : 1;
+      int got, it0, nit;
+      claim(A, chunk, got, it0, nit);
+      if (threadIdx.x == 0) {
+        s_sub = got;
+        s_it0 = it0;
+        s_nit = nit;
+        s_exit = 0;
+        if (got < 0) {
+          s_exit = *(volatile unsigned*)A.n_done >= (unsigned)A.nact;
+        } else {
+          __threadfence();   // acquire
+          s_act = load_act(A, got);
+          if (A.probe && got == A.probe_sub && it0 + nit == A.geo[got].nitems) {
+            unsigned long long now;   // LAST chunk of the action claimed
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            const unsigned long long sq = (*(volatile unsigned long long*)&A.ctl[got].word) >> 32;
+            A.probe[(sq % (unsigned long long)A.probe_cap) * 4 + 1] = now;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_sub < 0) {
+      if (s_exit) break;
+      if (tid == 0) __nanosleep(backoff);
+      backoff = backoff < 256 ? backoff * 2 : 256;
+      __syncthreads();
+      continue;
+    }
+    backoff = 32;
+    const Act t = s_act;
+    const int l = t.sub;
+    const int it0 = s_it0, nit = s_nit;
+    const SubGeo& g = A.geo[l];
+    Acc acc{0u, 0u, 0.0, 0.0};
+    dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
+    const int any = __syncthreads_or(acc.flag);
+    const int anynf = __syncthreads_or(acc.nonfin);
+    unsigned long long emax = 0ull;
+    if (t.mode == M_FINAL)
+      emax = block_max_u64((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
+    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
+    if (tid == 0) {
+      DevCtl* gc = A.ctl + l;
+      unsigned bits = 0;
+      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
+      if (anynf) bits |= 4u;
+      if (bits) atomicOr(&gc->acc_flags, bits);
+      if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
+      __threadfence();
+      const unsigned d = atomicAdd(&gc->done, (unsigned)nit);
+      s_last = d + (unsigned)nit == (unsigned)g.nitems;
+      if (s_last && A.probe && l == A.probe_sub) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        const unsigned long long sq = (*(volatile unsigned long long*)&gc->word) >> 32;
+        A.probe[(sq % (unsigned long long)A.probe_cap) * 4 + 2] = now;
+      }
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      double sum = 0.0;
+      if (sums) {
+        double v = 0.0;
+        for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
+        sum = block_sum(v, sh_sum);
+      }
+      if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
+    }
+    __syncthreads();
+  }
+}
+
 // Window start for the active subdomains (one thread each): phase F0 /
 // EULER, first action published.
 __global__ void k_window_begin(const WinArgs A) {
@@ -857,8 +1350,11 @@ int window_blocks(int dim, int pow2) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (dim == 2) {
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<2, true>, NT, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<2, false>, NT, 0);
+    const int smem = 2 * STAGE2_BYTES;
+    cudaFuncSetAttribute(k_window2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_window2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window2<true>, NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window2<false>, NT, smem);
   } else {
     if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, true>, NT, 0);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, false>, NT, 0);
@@ -876,9 +1372,14 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   const dim3 blk(TX, TY);
   void* args[] = {(void*)&a};
   void* fn;
-  if (a.P.dim == 2) fn = a.P.pow2 ? (void*)k_window<2, true> : (void*)k_window<2, false>;
-  else fn = a.P.pow2 ? (void*)k_window<3, true> : (void*)k_window<3, false>;
-  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, 0, (cudaStream_t)stream);
+  size_t smem = 0;
+  if (a.P.dim == 2) {
+    fn = a.P.pow2 ? (void*)k_window2<true> : (void*)k_window2<false>;
+    smem = 2 * STAGE2_BYTES;
+  } else {
+    fn = a.P.pow2 ? (void*)k_window<3, true> : (void*)k_window<3, false>;
+  }
+  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem, (cudaStream_t)stream);
 }
 
 }  // namespace ddpma

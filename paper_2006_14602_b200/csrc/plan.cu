@@ -783,6 +783,16 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   A.trace = p->d_trace;
   A.trace_n = p->d_trace_n;
   A.trace_cap = p->trace_cap;
+  A.chunk_bulk = getenv("DDPMA_CHUNK") ? atoi(getenv("DDPMA_CHUNK")) : 8;
+  static unsigned long long* d_probe = nullptr;
+  const char* pe = getenv("DDPMA_PROBE");
+  if (pe) {
+    A.probe_cap = 1 << 16;
+    if (!d_probe) cudaMalloc((void**)&d_probe, sizeof(unsigned long long) * 4 * A.probe_cap);
+    cudaMemsetAsync(d_probe, 0, sizeof(unsigned long long) * 4 * A.probe_cap, p->st);
+    A.probe = d_probe;
+    A.probe_sub = order[0];
+  }
   launch_window_begin(A, p->st);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (p->prof) {
@@ -832,6 +842,23 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
         p->fail.nnodes = c.fail_nonfin ? -1 : -2;
       }
     }
+  }
+  if (pe) {
+    std::vector<unsigned long long> pr(4 * (size_t)A.probe_cap);
+    cudaMemcpy(pr.data(), d_probe, sizeof(unsigned long long) * pr.size(), cudaMemcpyDeviceToHost);
+    double s_wait = 0, s_proc = 0, s_dec = 0;
+    long n = 0;
+    for (int i = 0; i < A.probe_cap; ++i) {
+      const unsigned long long* r = &pr[4 * (size_t)i];
+      if (r[0] && r[1] && r[2] && r[3] && r[1] >= r[0] && r[2] >= r[1] && r[3] >= r[2]) {
+        s_wait += (r[1] - r[0]) * 1e-3;
+        s_proc += (r[2] - r[1]) * 1e-3;
+        s_dec += (r[3] - r[2]) * 1e-3;
+        ++n;
+      }
+    }
+    fprintf(stderr, "PROBE sub %d actions %ld: avg publish->claim %.2f us, claim->done %.2f us, done->published %.2f us\n",
+            p->local[A.probe_sub], n, n ? s_wait / n : 0.0, n ? s_proc / n : 0.0, n ? s_dec / n : 0.0);
   }
   if (getenv("DDPMA_TIMELINE")) {
     unsigned long long t0 = ~0ull;

@@ -188,6 +188,15 @@ def gen_runs(quick=False):
     run_save("C1_tol_max", lambda: ddmesh.solve(
         rg, rd, m1, ddmesh.SolverConfig(tol=1e-7, transmission="alternating",
                                          stop_rule="max")))
+    # tight-tolerance ("stable") profile: non-chaotic trajectories
+    run_save(f"C1_alternating_stable_{nwin}", lambda: ddmesh.solve(
+        rg, rd, m1, cfg(max_windows=nwin, transmission="alternating", rtol=1e-6, atol=1e-9)))
+    run_save(f"C1_single_stable_{nwin}", lambda: ddmesh.solve_single_domain(
+        rg, m1, cfg(max_windows=nwin, rtol=1e-6, atol=1e-9)))
+    for rule in ("min", "max"):
+        run_save(f"C1_stabletol_{rule}", lambda: ddmesh.solve(
+            rg, rd, m1, ddmesh.SolverConfig(tol=1e-7, transmission="parallel", stop_rule=rule,
+                                             rtol=1e-6, atol=1e-9)))
     # parallel transmission to convergence under the tight-tolerance profile
     run_save(f"C1_parallel_stable_{nwin}", lambda: ddmesh.solve(
         rg, rd, m1, cfg(max_windows=nwin, transmission="parallel", rtol=1e-6, atol=1e-9)))
