@@ -50,6 +50,7 @@ struct Prob {
   double measure;        // global |Omega_c| (grid.py:41-47)
   double floor;          // det_floor
   double guard;          // max(floor, 0.1/(measure*rho_max)) (pma.py:188-190)
+  double rguard;         // RN(1/guard) for the exact det/guard (stencil.cuh saturate)
   double atol, rtol;
   double a0[3];          // extents[k][0]
 };
@@ -82,7 +83,7 @@ struct SubGeo {
 };
 
 constexpr int IR2 = 16;   // 2D work item: TX x IR2 nodes (each thread IR2/TY rows)
-constexpr int IZ3 = 8;    // 3D work item: TX x TY x IZ3 nodes
+constexpr int IZ3 = 2;    // 3D work item: TX x TY x IZ3 nodes
 
 // One participant (local subdomain) of a batched launch: its action (mode),
 // buffers and the scalars of that action.

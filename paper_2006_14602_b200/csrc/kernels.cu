@@ -63,7 +63,7 @@ __device__ __forceinline__ void eval_cta(const KArgs& a, const Entry& e, int b) 
       } else {
         det = hdet<DIM, P2>(a.P, g, i0, i1, i2, YAcc<DIM, YM_SEED>{&g, yb, nullptr, e.c});
       }
-      const double F = dir ? 0.0 : logequi(__ldg(a.F.mr + k), det, a.P.guard, a.P.floor);
+      const double F = dir ? 0.0 : logequi(__ldg(a.F.mr + k), det, a.P.guard, a.P.floor, a.P.rguard);
       flag = (det <= a.P.floor && !dir) ? 1u : 0u;
       if constexpr (MODE == M_F0) {
         a.F.f[e.fi][k] = F;

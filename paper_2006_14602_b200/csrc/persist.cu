@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "ddpma_internal.h"
 #include "stencil.cuh"
@@ -124,7 +125,7 @@ __device__ __forceinline__ void node(const WinArgs& A, const SubGeo& g, const Ac
     double det;
     if (interior) det = hdet<DIM, P2>(A.P, g, i0, i1, i2, S);
     else det = hdet<DIM, P2>(A.P, g, i0, i1, i2, GAcc<DIM, YM>{&g, yb, aptr, t.c});
-    const double F = dir ? 0.0 : logequi(ldc(A.F.mr + k), det, A.P.guard, A.P.floor);
+    const double F = dir ? 0.0 : logequi(ldc(A.F.mr + k), det, A.P.guard, A.P.floor, A.P.rguard);
     acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
     if constexpr (MODE == M_F0) {
       A.F.f[t.fi][k] = F;
@@ -253,7 +254,7 @@ __device__ void item2(const WinArgs& A, const SubGeo& g, const Act& t, int item,
       double det;
       if (interior) det = hdet2_fast<P2>(A.P, sY + (threadIdx.y + q * TY + 1) * W + threadIdx.x + 1);
       else det = hdet<2, P2>(A.P, g, i0, i1, 0, GAcc<2, YM>{&g, yb, ap, t.c});
-      const double F = dir ? 0.0 : logequi(cm[q], det, A.P.guard, A.P.floor);
+      const double F = dir ? 0.0 : logequi(cm[q], det, A.P.guard, A.P.floor, A.P.rguard);
       acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
       if constexpr (MODE == M_F0) {
         A.F.f[t.fi][k] = F;
@@ -863,10 +864,8 @@ __device__ __forceinline__ void cpa_wait() {
 }
 
 template <int MODE, int YM>
-__device__ __forceinline__ void issue2(const WinArgs& A, const SubGeo& g, const Act& t, int item,
-                                       Stage2& st) {
-  const int ix = item % g.items_x, iy = item / g.items_x;
-  const int c0 = ix * TX, r0 = iy * IR2;
+__device__ __forceinline__ void issue2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+                                       int r0, Stage2& st) {
   const double* yb = A.F.y[t.yi];
   const double* ap = nullptr;
   if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
@@ -942,14 +941,12 @@ struct TileAcc2 {
 };
 
 template <bool P2, int MODE, int YM>
-__device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int item,
-                                         const Stage2& st, Acc& acc, double* psum_item) {
+__device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+                                         int r0, const Stage2& st, Acc& acc, double* psum_item) {
   constexpr int R = IR2 / TY;
   // how Y is formed from global memory (outside the tile) for this mode
   constexpr int YMG = MODE == M_STAGE2 ? YM_SCALED
                       : (MODE == M_STAGE3 || MODE == M_STAGEN) ? YM_ADD : YM;
-  const int ix = item % g.items_x, iy = item / g.items_x;
-  const int c0 = ix * TX, r0 = iy * IR2;
   const int n0 = g.n[0], n1 = g.n[1];
   const int i1 = c0 + threadIdx.x;
   const double* yb = A.F.y[t.yi];
@@ -1021,7 +1018,7 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
       const int i0 = r0 + lr;
       const bool dir = ((edge >> q) & 1u) && dirichlet<2>(g, i0, i1, 0);   // faces only
       const int pc = lr * TX + threadIdx.x;
-      F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor);
+      F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor, A.P.rguard);
       acc.flag |= ((valid >> q) & 1u) && det[q] <= A.P.floor && !dir ? 1u : 0u;
     }
     // phase 4: epilogues
@@ -1182,10 +1179,17 @@ template <bool P2, int MODE, int YM>
 __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
                        Stage2* stage, Acc& acc, double* sh_sum) {
   constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
-  issue2<MODE, YM>(A, g, t, it0, stage[0]);
+  // item -> (column, row) tile origin, decoded once per chunk then stepped
+  int ix = it0 % g.items_x, iy = it0 / g.items_x;
+  int nx = ix + 1, ny = iy;
+  if (nx == g.items_x) {
+    nx = 0;
+    ++ny;
+  }
+  issue2<MODE, YM>(A, g, t, ix * TX, iy * IR2, stage[0]);
   for (int i = 0; i < nit; ++i) {
     if (i + 1 < nit) {
-      issue2<MODE, YM>(A, g, t, it0 + i + 1, stage[(i + 1) & 1]);
+      issue2<MODE, YM>(A, g, t, nx * TX, ny * IR2, stage[(i + 1) & 1]);
       cpa_wait<1>();
     } else {
       cpa_wait<0>();
@@ -1204,7 +1208,14 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     }
     double ps = 0.0;
     constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
-    compute2<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, it0 + i, stage[i & 1], acc, &ps);
+    compute2<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, ix * TX, iy * IR2, stage[i & 1], acc,
+                                                 &ps);
+    ix = nx;
+    iy = ny;
+    if (++nx == g.items_x) {
+      nx = 0;
+      ++ny;
+    }
     if constexpr (SUMS) {
       const double s = block_sum(ps, sh_sum);   // per-item partial: deterministic
       if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, s);
@@ -1231,10 +1242,270 @@ __device__ void dispatch_chunk2(const WinArgs& A, const SubGeo& g, const Act& t,
   }
 }
 
+// ----------------------------------------------------------------- 3D ----
+// Same pipeline for 3D boxes: items of TX x TY x IZ3 nodes (32 x 8 x 2); the
+// stage holds the (IZ3+2) x (TY+2) x 36 halo tiles of y and a plus the centre
+// fields.  The interior Hessian is the 19-point formula of hdet<3>.
+constexpr int TH3 = TY + 2, TD3 = IZ3 + 2;
+constexpr int SY3 = TW2, SZ3 = TH3 * TW2;
+struct Stage3 {
+  double ys[TD3 * TH3 * TW2];
+  double as[TD3 * TH3 * TW2];
+  double cm[IZ3 * TY * TX];
+  double cf[IZ3 * TY * TX];
+  double cd[IZ3 * TY * TX];
+};
+
+template <int MODE, int YM>
+__device__ __forceinline__ void issue3(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+                                       int r0, int z0, Stage3& st) {
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  constexpr bool HAS_A = YM == YM_ADD || YM == YM_SCALED;
+  constexpr bool NEED_F0 = MODE == M_STAGE3 || MODE == M_STAGEN || MODE == M_FINAL ||
+                           MODE == M_POWER || MODE == M_POWER_SEED;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  constexpr int CH = TW2 / 2;
+  const long long plane = (long long)g.n[1] * g.pitch;
+  for (int e = tid; e < TD3 * TH3 * CH; e += NT) {
+    const int cc = e % CH, rr = (e / CH) % TH3, zz = e / (CH * TH3);
+    const int i0 = z0 - 1 + zz, i1 = r0 - 1 + rr, col = c0 - 2 + 2 * cc;
+    const bool ok = i0 >= 0 && i0 < g.n[0] && i1 >= 0 && i1 < g.n[1] && col >= 0 && col < g.pitch;
+    const long long k = ok ? g.off + i0 * plane + (long long)i1 * g.pitch + col : g.off;
+    const int sidx = (zz * TH3 + rr) * TW2 + 2 * cc;
+    cpa16(&st.ys[sidx], yb + k, ok ? 16 : 0);
+    if constexpr (HAS_A) cpa16(&st.as[sidx], ap + k, ok ? 16 : 0);
+  }
+  if constexpr (MODE != M_NORM) {
+    constexpr int CC = TX / 2;
+    for (int e = tid; e < IZ3 * TY * CC; e += NT) {
+      const int cc = e % CC, rr = (e / CC) % TY, zz = e / (CC * TY);
+      const int i0 = z0 + zz, i1 = r0 + rr, col = c0 + 2 * cc;
+      const bool ok = i0 < g.n[0] && i1 < g.n[1] && col < g.pitch;
+      const long long k = ok ? g.off + i0 * plane + (long long)i1 * g.pitch + col : g.off;
+      const int cidx = (zz * TY + rr) * TX + 2 * cc;
+      cpa16(&st.cm[cidx], A.F.mr + k, ok ? 16 : 0);
+      if constexpr (NEED_F0) cpa16(&st.cf[cidx], A.F.f[t.fi] + k, ok ? 16 : 0);
+      if constexpr (MODE == M_STAGEN) cpa16(&st.cd[cidx], A.F.d[(t.j - 2) % 3] + k, ok ? 16 : 0);
+    }
+  }
+  cpa_commit();
+}
+
+template <int YM, int YMG = YM>
+struct TileAcc3 {
+  const Stage3* st;
+  int z0, r0, c0;
+  GAcc<3, YMG> g;
+  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
+    const int zz = i0 - z0 + 1, rr = i1 - r0 + 1, cc = i2 - c0 + 2;
+    if (zz >= 0 && zz < TD3 && rr >= 0 && rr < TH3 && cc >= 0 && cc < TW2) {
+      const int p = (zz * TH3 + rr) * TW2 + cc;
+      if constexpr (YM == YM_PLAIN) {
+        return st->ys[p];
+      } else if constexpr (YM == YM_ADD) {
+        return st->ys[p] + st->as[p];
+      } else if constexpr (YM == YM_SCALED) {
+        return st->ys[p] + g.c * st->as[p];
+      } else {
+        return st->ys[p] + (((i0 + i1 + i2) & 1) ? -g.c : g.c);
+      }
+    }
+    return g(i0, i1, i2);
+  }
+};
+
+template <int YM>
+__device__ __forceinline__ double yat3(const Stage3& st, int p, double c, int par) {
+  if constexpr (YM == YM_PLAIN) {
+    return st.ys[p];
+  } else if constexpr (YM == YM_ADD) {
+    return st.ys[p] + st.as[p];
+  } else if constexpr (YM == YM_SCALED) {
+    return st.ys[p] + c * st.as[p];
+  } else {
+    return st.ys[p] + (par ? -c : c);
+  }
+}
+
+template <bool P2, int MODE, int YM>
+__device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+                                         int r0, int z0, const Stage3& st, Acc& acc,
+                                         double* psum_item) {
+  constexpr int YMG = MODE == M_STAGE2 ? YM_SCALED
+                      : (MODE == M_STAGE3 || MODE == M_STAGEN) ? YM_ADD : YM;
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const int i1 = r0 + threadIdx.y, i2 = c0 + threadIdx.x;
+  const double* yb = A.F.y[t.yi];
+  const double* ap = nullptr;
+  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
+  const long long plane = (long long)n1 * g.pitch;
+  double ps = 0.0;
+#pragma unroll
+  for (int q = 0; q < IZ3; ++q) {
+    const int i0 = z0 + q;
+    if (i0 >= n0 || i1 >= n1 || i2 >= n2) continue;
+    const int p = ((q + 1) * TH3 + threadIdx.y + 1) * TW2 + threadIdx.x + 2;
+    const int pc = (q * TY + threadIdx.y) * TX + threadIdx.x;
+    const long long k = g.off + i0 * plane + (long long)i1 * g.pitch + i2;
+    if constexpr (MODE == M_NORM) {
+      const double y = st.ys[p];
+      ps += y * y;
+      continue;
+    } else {
+      const bool interior = i0 >= 1 && i0 <= n0 - 2 && i1 >= 1 && i1 <= n1 - 2 && i2 >= 1 &&
+                            i2 <= n2 - 2;
+      double det;
+      if (interior) {
+        const int par = (i0 + i1 + i2) & 1;
+        const double c = yat3<YM>(st, p, t.c, par);
+        const double h00 = dv<P2>((yat3<YM>(st, p + SZ3, t.c, par ^ 1) - 2.0 * c) +
+                                      yat3<YM>(st, p - SZ3, t.c, par ^ 1),
+                                  A.P.ax[0].hh, A.P.ax[0].ihh);
+        const double h11 = dv<P2>((yat3<YM>(st, p + SY3, t.c, par ^ 1) - 2.0 * c) +
+                                      yat3<YM>(st, p - SY3, t.c, par ^ 1),
+                                  A.P.ax[1].hh, A.P.ax[1].ihh);
+        const double h22 = dv<P2>((yat3<YM>(st, p + 1, t.c, par ^ 1) - 2.0 * c) +
+                                      yat3<YM>(st, p - 1, t.c, par ^ 1),
+                                  A.P.ax[2].hh, A.P.ax[2].ihh);
+        double gp = dv<P2>(yat3<YM>(st, p + SZ3 + SY3, t.c, par) -
+                               yat3<YM>(st, p + SZ3 - SY3, t.c, par),
+                           A.P.ax[1].twoh, A.P.ax[1].itwoh);
+        double gm = dv<P2>(yat3<YM>(st, p - SZ3 + SY3, t.c, par) -
+                               yat3<YM>(st, p - SZ3 - SY3, t.c, par),
+                           A.P.ax[1].twoh, A.P.ax[1].itwoh);
+        const double h01 = dv<P2>(gp - gm, A.P.ax[0].twoh, A.P.ax[0].itwoh);
+        gp = dv<P2>(yat3<YM>(st, p + SZ3 + 1, t.c, par) - yat3<YM>(st, p + SZ3 - 1, t.c, par),
+                    A.P.ax[2].twoh, A.P.ax[2].itwoh);
+        gm = dv<P2>(yat3<YM>(st, p - SZ3 + 1, t.c, par) - yat3<YM>(st, p - SZ3 - 1, t.c, par),
+                    A.P.ax[2].twoh, A.P.ax[2].itwoh);
+        const double h02 = dv<P2>(gp - gm, A.P.ax[0].twoh, A.P.ax[0].itwoh);
+        gp = dv<P2>(yat3<YM>(st, p + SY3 + 1, t.c, par) - yat3<YM>(st, p + SY3 - 1, t.c, par),
+                    A.P.ax[2].twoh, A.P.ax[2].itwoh);
+        gm = dv<P2>(yat3<YM>(st, p - SY3 + 1, t.c, par) - yat3<YM>(st, p - SY3 - 1, t.c, par),
+                    A.P.ax[2].twoh, A.P.ax[2].itwoh);
+        const double h12 = dv<P2>(gp - gm, A.P.ax[1].twoh, A.P.ax[1].itwoh);
+        det = (h00 * (h11 * h22 - h12 * h12) - h01 * (h01 * h22 - h12 * h02)) +
+              h02 * (h01 * h12 - h11 * h02);
+      } else {
+        det = hdet<3, P2>(A.P, g, i0, i1, i2,
+                          TileAcc3<YM, YMG>{&st, z0, r0, c0, GAcc<3, YMG>{&g, yb, ap, t.c}});
+      }
+      const bool dir = !interior && dirichlet<3>(g, i0, i1, i2);
+      const double F = dir ? 0.0 : logequi(st.cm[pc], det, A.P.guard, A.P.floor, A.P.rguard);
+      acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
+      if constexpr (MODE == M_F0) {
+        A.F.f[t.fi][k] = F;
+      } else if constexpr (MODE == M_EULER) {
+        A.F.y[1 - t.yi][k] = st.ys[p] + t.c * F;
+      } else if constexpr (MODE == M_STAGE2) {
+        const double f0 = st.as[p];
+        const double d1 = t.c * f0;
+        A.F.d[2][k] = ((t.mu * d1 + t.nu * 0.0) + t.hmut * F) + t.hgt * f0;
+      } else if constexpr (MODE == M_STAGE3) {
+        const double f0 = st.cf[pc];
+        const double d1 = t.c * f0;
+        A.F.d[0][k] = ((t.mu * st.as[p] + t.nu * d1) + t.hmut * F) + t.hgt * f0;
+      } else if constexpr (MODE == M_STAGEN) {
+        const double f0 = st.cf[pc];
+        A.F.d[t.j % 3][k] = ((t.mu * st.as[p] + t.nu * st.cd[pc]) + t.hmut * F) + t.hgt * f0;
+      } else if constexpr (MODE == M_FINAL) {
+        const double ds = st.as[p], yv = st.ys[p], f0 = st.cf[pc];
+        const double yn = yv + ds;
+        A.F.f[1 - t.fi][k] = F;
+        A.F.y[1 - t.yi][k] = yn;
+        const double err = -0.8 * ds + t.h04 * (f0 + F);
+        const double ay = fabs(yv), an = fabs(yn);
+        const double mx = (ay >= an || isnan(ay)) ? ay : an;
+        const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
+        if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
+        else acc.nonfin = 1;
+      } else {
+        const double diff = F - st.cf[pc];
+        A.F.d[t.vout][k] = diff;
+        ps += diff * diff;
+      }
+    }
+  }
+  *psum_item = ps;
+}
+
+template <bool P2, int MODE, int YM>
+__device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
+                       Stage3* stage, Acc& acc, double* sh_sum) {
+  constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
+  auto origin = [&](int item, int& c0, int& r0, int& z0) {
+    const int ix = item % g.items_x;
+    const int rest = item / g.items_x;
+    c0 = ix * TX;
+    r0 = (rest % g.items_y) * TY;
+    z0 = (rest / g.items_y) * IZ3;
+  };
+  int c0, r0, z0, nc0 = 0, nr0 = 0, nz0 = 0;
+  origin(it0, c0, r0, z0);
+  issue3<MODE, YM>(A, g, t, c0, r0, z0, stage[0]);
+  for (int i = 0; i < nit; ++i) {
+    if (i + 1 < nit) {
+      origin(it0 + i + 1, nc0, nr0, nz0);
+      issue3<MODE, YM>(A, g, t, nc0, nr0, nz0, stage[(i + 1) & 1]);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
+    if constexpr (COMBINED) {
+      Stage3& sg = stage[i & 1];
+      const int tid = threadIdx.y * TX + threadIdx.x;
+      for (int e = tid; e < TD3 * TH3 * TW2; e += NT) {
+        if constexpr (YM == YM_ADD) sg.ys[e] = sg.ys[e] + sg.as[e];
+        else sg.ys[e] = sg.ys[e] + t.c * sg.as[e];
+      }
+      __syncthreads();
+    }
+    double ps = 0.0;
+    compute3<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, c0, r0, z0, stage[i & 1], acc, &ps);
+    if constexpr (SUMS) {
+      const double s = block_sum(ps, sh_sum);
+      if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, s);
+    } else {
+      __syncthreads();
+    }
+    c0 = nc0;
+    r0 = nr0;
+    z0 = nz0;
+  }
+}
+
 template <bool P2>
-__global__ void __launch_bounds__(NT, 4) k_window2(const WinArgs A) {
+__device__ void dispatch_chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
+                                Stage3* st, Acc& acc, double* sh) {
+  switch (t.mode) {
+    case M_F0: chunk3<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_EULER: chunk3<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGE2: chunk3<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGE3: chunk3<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_STAGEN: chunk3<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_FINAL: chunk3<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_POWER: chunk3<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_POWER_SEED: chunk3<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_NORM: chunk3<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    default: break;
+  }
+}
+
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 3) k_windowP(const WinArgs A) {
+  using Stage = typename std::conditional<DIM == 2, Stage2, Stage3>::type;
   extern __shared__ __align__(16) unsigned char dsm[];
-  Stage2* stage = reinterpret_cast<Stage2*>(dsm);
+  Stage* stage = reinterpret_cast<Stage*>(dsm);
   __shared__ double sh_sum[NT / 32];
   __shared__ unsigned long long sh_max[NT / 32];
   __shared__ Act s_act;
@@ -1282,7 +1553,8 @@ __global__ void __launch_bounds__(NT, 4) k_window2(const WinArgs A) {
     const int it0 = s_it0, nit = s_nit;
     const SubGeo& g = A.geo[l];
     Acc acc{0u, 0u, 0.0, 0.0};
-    dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
+    if constexpr (DIM == 2) dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
+    else dispatch_chunk3<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
     const int any = __syncthreads_or(acc.flag);
     const int anynf = __syncthreads_or(acc.nonfin);
     unsigned long long emax = 0ull;
@@ -1351,13 +1623,16 @@ int window_blocks(int dim, int pow2) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (dim == 2) {
     const int smem = 2 * STAGE2_BYTES;
-    cudaFuncSetAttribute(k_window2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_window2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window2<true>, NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window2<false>, NT, smem);
+    cudaFuncSetAttribute(k_windowP<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_windowP<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, true>, NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, false>, NT, smem);
   } else {
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, true>, NT, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_window<3, false>, NT, 0);
+    const int smem = 2 * (int)sizeof(Stage3);
+    cudaFuncSetAttribute(k_windowP<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_windowP<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<3, true>, NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<3, false>, NT, smem);
   }
   return sms * (per > 0 ? per : 1);
 }
@@ -1374,10 +1649,11 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   void* fn;
   size_t smem = 0;
   if (a.P.dim == 2) {
-    fn = a.P.pow2 ? (void*)k_window2<true> : (void*)k_window2<false>;
+    fn = a.P.pow2 ? (void*)k_windowP<2, true> : (void*)k_windowP<2, false>;
     smem = 2 * STAGE2_BYTES;
   } else {
-    fn = a.P.pow2 ? (void*)k_window<3, true> : (void*)k_window<3, false>;
+    fn = a.P.pow2 ? (void*)k_windowP<3, true> : (void*)k_windowP<3, false>;
+    smem = 2 * sizeof(Stage3);
   }
   cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem, (cudaStream_t)stream);
 }

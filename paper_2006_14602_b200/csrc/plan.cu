@@ -953,6 +953,7 @@ void set_guard(ddpma_plan* p, double rho_max) {     // pma.py:188-190
   double guard = p->cfg.det_floor;
   if (rho_max != 0.0) guard = std::max(p->cfg.det_floor, 0.1 / (p->P.measure * rho_max));
   p->P.guard = guard;
+  p->P.rguard = 1.0 / guard;
 }
 
 // snapshot + measure*rho for the listed local subdomains
@@ -1288,6 +1289,7 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   P.measure = grid->explicit_geom ? grid->measure : measure;
   P.floor = cfg->det_floor;
   P.guard = cfg->det_floor;
+  P.rguard = 1.0 / cfg->det_floor;
   P.atol = cfg->atol;
   P.rtol = cfg->rtol;
   // monitor

@@ -1,5 +1,7 @@
 """Run W warm-up windows of a BASELINE config, then one more window (the one
-ncu captures with -k regex:k_window -s W)."""
+ncu captures with -k k_windowP -s W).  Prints the node-updates and algorithmic
+bytes of every window (exact controller tallies) as JSON lines."""
+import json
 import sys
 sys.path.insert(0, ".")
 import paper_2006_14602_b200 as P
@@ -10,6 +12,10 @@ W = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 g, d, m = bench.case(name, P)
 plan = Plan.for_grid(g, d.subdomains, m, P.SolverConfig(tol=1e-300, max_windows=W + 1, transmission="parallel"))
 plan.set_state(None)
+prev = plan.counters()
 for w in range(W + 1):
     plan.run(1, 1e-300)
-print("done", plan.counters())
+    c = plan.counters()
+    print(json.dumps({"window": w, "node_updates": c["node_updates"] - prev["node_updates"],
+                      "algo_bytes": c["algo_bytes"] - prev["algo_bytes"]}), flush=True)
+    prev = c
