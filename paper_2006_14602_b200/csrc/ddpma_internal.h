@@ -203,7 +203,11 @@ struct WinArgs {
   unsigned long long* probe;   // debug: [cap][4] = publish, first claim, last done, decided
   int probe_sub, probe_cap;
   int chunk_bulk;            // items per claim while >= 16 subdomains are active
+  const void* tmap;          // 2D: CUtensorMap[nlocal][8 fields][2 boxes] (TMA tile loads), or null
 };
+
+// fields addressable by the window kernel's tensor maps
+enum { TF_Y0 = 0, TF_Y1, TF_F0, TF_F1, TF_D0, TF_D1, TF_D2, TF_MR, TF_N };
 
 void launch_window(const WinArgs& a, int nblocks, void* stream);
 int window_blocks(int dim, int pow2);   // co-resident CTAs for the cooperative launch

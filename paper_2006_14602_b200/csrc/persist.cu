@@ -843,9 +843,10 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A
 
 constexpr int TW2 = TX + 4;    // 36 doubles: columns c0-2 .. c0+33 (16-B aligned chunks)
 constexpr int TH2 = IR2 + 2;   // 34 rows
+constexpr int HALO2 = (TH2 * TW2 + 15) / 16 * 16;   // 128-B multiple (TMA destinations)
 struct Stage2 {
-  double ys[TH2 * TW2];
-  double as[TH2 * TW2];
+  double ys[HALO2];
+  double as[HALO2];
   double cm[IR2 * TX];
   double cf[IR2 * TX];
   double cd[IR2 * TX];
@@ -899,6 +900,67 @@ __device__ __forceinline__ void issue2(const WinArgs& A, const SubGeo& g, const 
     }
   }
   cpa_commit();
+}
+
+// ---- TMA (cp.async.bulk.tensor) tile loads, completion on an mbarrier ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma2(void* dst, const void* tmap, int x, int y,
+                                     unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(m))
+      : "memory");
+}
+
+// One thread: the TMA copies of one 2D item into stage `st` (zero fill outside the box).
+template <int MODE, int YM>
+__device__ __forceinline__ void issue2_tma(const WinArgs& A, int l, const Act& t, int c0, int r0,
+                                           Stage2& st, unsigned long long* mbar) {
+  constexpr bool HAS_A = YM == YM_ADD || YM == YM_SCALED;
+  constexpr bool NEED_F0 = MODE == M_STAGE3 || MODE == M_STAGEN || MODE == M_FINAL ||
+                           MODE == M_POWER || MODE == M_POWER_SEED;
+  int fa = 0;
+  if constexpr (MODE == M_STAGE2) fa = TF_F0 + t.fi;
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) fa = TF_D0 + (t.j - 1) % 3;
+  if constexpr (MODE == M_FINAL) fa = TF_D0 + t.s % 3;
+  if constexpr (MODE == M_POWER) fa = TF_D0 + t.vin;
+  const char* tm = reinterpret_cast<const char*>(A.tmap) + (size_t)l * TF_N * 2 * 128;
+  auto map = [&](int f, int kind) { return tm + (f * 2 + kind) * 128; };
+  unsigned bytes = TH2 * TW2 * 8;
+  if constexpr (HAS_A) bytes += TH2 * TW2 * 8;
+  if constexpr (MODE != M_NORM) {
+    bytes += IR2 * TX * 8;
+    if constexpr (NEED_F0) bytes += IR2 * TX * 8;
+    if constexpr (MODE == M_STAGEN) bytes += IR2 * TX * 8;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  mbar_expect(mbar, bytes);
+  tma2(st.ys, map(TF_Y0 + t.yi, 0), c0 - 2, r0 - 1, mbar);
+  if constexpr (HAS_A) tma2(st.as, map(fa, 0), c0 - 2, r0 - 1, mbar);
+  if constexpr (MODE != M_NORM) {
+    tma2(st.cm, map(TF_MR, 1), c0, r0, mbar);
+    if constexpr (NEED_F0) tma2(st.cf, map(TF_F0 + t.fi, 1), c0, r0, mbar);
+    if constexpr (MODE == M_STAGEN) tma2(st.cd, map(TF_D0 + (t.j - 2) % 3, 1), c0, r0, mbar);
+  }
 }
 
 template <int YM>
@@ -1177,7 +1239,8 @@ __device__ void decide(const WinArgs& A, int l, const SubGeo& g, double sum, Dev
 
 template <bool P2, int MODE, int YM>
 __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
-                       Stage2* stage, Acc& acc, double* sh_sum) {
+                       Stage2* stage, Acc& acc, double* sh_sum, unsigned long long* mbar,
+                       unsigned& phases) {
   constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
   // item -> (column, row) tile origin, decoded once per chunk then stepped
   int ix = it0 % g.items_x, iy = it0 / g.items_x;
@@ -1186,15 +1249,29 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     nx = 0;
     ++ny;
   }
-  issue2<MODE, YM>(A, g, t, ix * TX, iy * IR2, stage[0]);
+  const bool tma = A.tmap != nullptr;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (tma) {
+    if (lead) issue2_tma<MODE, YM>(A, t.sub, t, ix * TX, iy * IR2, stage[0], &mbar[0]);
+  } else {
+    issue2<MODE, YM>(A, g, t, ix * TX, iy * IR2, stage[0]);
+  }
   for (int i = 0; i < nit; ++i) {
-    if (i + 1 < nit) {
-      issue2<MODE, YM>(A, g, t, nx * TX, ny * IR2, stage[(i + 1) & 1]);
-      cpa_wait<1>();
+    const int s = i & 1;
+    if (tma) {
+      if (i + 1 < nit && lead)
+        issue2_tma<MODE, YM>(A, t.sub, t, nx * TX, ny * IR2, stage[s ^ 1], &mbar[s ^ 1]);
+      mbar_wait(&mbar[s], (phases >> s) & 1u);
+      phases ^= 1u << s;
     } else {
-      cpa_wait<0>();
+      if (i + 1 < nit) {
+        issue2<MODE, YM>(A, g, t, nx * TX, ny * IR2, stage[s ^ 1]);
+        cpa_wait<1>();
+      } else {
+        cpa_wait<0>();
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
       // Y = y + d (or y + c*f0) once per tile point instead of 9x per node;
       // the centre of the a tile (d_{j-1} / f0) stays intact for the epilogue
@@ -1227,17 +1304,20 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
 
 template <bool P2>
 __device__ void dispatch_chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
-                                Stage2* st, Acc& acc, double* sh) {
+                                Stage2* st, Acc& acc, double* sh, unsigned long long* mb,
+                                unsigned& ph) {
   switch (t.mode) {
-    case M_F0: chunk2<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_EULER: chunk2<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGE2: chunk2<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGE3: chunk2<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGEN: chunk2<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_FINAL: chunk2<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_POWER: chunk2<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_POWER_SEED: chunk2<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_NORM: chunk2<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_F0: chunk2<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_EULER: chunk2<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGE2: chunk2<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGE3: chunk2<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGEN: chunk2<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_FINAL: chunk2<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_POWER: chunk2<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_POWER_SEED:
+      chunk2<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh, mb, ph);
+      break;
+    case M_NORM: chunk2<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
     default: break;
   }
 }
@@ -1504,8 +1584,17 @@ __device__ void dispatch_chunk3(const WinArgs& A, const SubGeo& g, const Act& t,
 template <int DIM, bool P2>
 __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 3) k_windowP(const WinArgs A) {
   using Stage = typename std::conditional<DIM == 2, Stage2, Stage3>::type;
-  extern __shared__ __align__(16) unsigned char dsm[];
-  Stage* stage = reinterpret_cast<Stage*>(dsm);
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Stage* stage = reinterpret_cast<Stage*>(
+      dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
+  __shared__ __align__(8) unsigned long long s_mbar[2];
+  unsigned phases = 0u;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    mbar_init(&s_mbar[0]);
+    mbar_init(&s_mbar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   __shared__ double sh_sum[NT / 32];
   __shared__ unsigned long long sh_max[NT / 32];
   __shared__ Act s_act;
@@ -1553,7 +1642,8 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 3) k_windowP(const WinArgs 
     const int it0 = s_it0, nit = s_nit;
     const SubGeo& g = A.geo[l];
     Acc acc{0u, 0u, 0.0, 0.0};
-    if constexpr (DIM == 2) dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
+    if constexpr (DIM == 2)
+      dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_mbar, phases);
     else dispatch_chunk3<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
     const int any = __syncthreads_or(acc.flag);
     const int anynf = __syncthreads_or(acc.nonfin);
@@ -1622,13 +1712,13 @@ int window_blocks(int dim, int pow2) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (dim == 2) {
-    const int smem = 2 * STAGE2_BYTES;
+    const int smem = 2 * STAGE2_BYTES + 128;
     cudaFuncSetAttribute(k_windowP<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_windowP<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, true>, NT, smem);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, false>, NT, smem);
   } else {
-    const int smem = 2 * (int)sizeof(Stage3);
+    const int smem = 2 * (int)sizeof(Stage3) + 128;
     cudaFuncSetAttribute(k_windowP<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_windowP<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<3, true>, NT, smem);
@@ -1650,10 +1740,10 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   size_t smem = 0;
   if (a.P.dim == 2) {
     fn = a.P.pow2 ? (void*)k_windowP<2, true> : (void*)k_windowP<2, false>;
-    smem = 2 * STAGE2_BYTES;
+    smem = 2 * STAGE2_BYTES + 128;
   } else {
     fn = a.P.pow2 ? (void*)k_windowP<3, true> : (void*)k_windowP<3, false>;
-    smem = 2 * sizeof(Stage3);
+    smem = 2 * sizeof(Stage3) + 128;
   }
   cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem, (cudaStream_t)stream);
 }

@@ -10,6 +10,7 @@
 // subdomain.  Host scalar arithmetic is compiled with -ffp-contract=off so it
 // rounds exactly like the reference's Python floats.
 
+#include <cuda.h>   // CUtensorMap / cuTensorMapEncodeTiled types (entry point fetched at run time)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -188,6 +189,7 @@ struct ddpma_plan {
   int trace_cap = 0;
   int win_blocks = 0;
   bool host_ctl = false;
+  void* d_tmap = nullptr;                  // 2D TMA tensor maps (persist.cu issue2_tma)
   std::vector<long long> last_evals;       // per local subdomain, previous window
   long long mode_nodes[9] = {0};
 };
@@ -784,6 +786,7 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   A.trace_n = p->d_trace_n;
   A.trace_cap = p->trace_cap;
   A.chunk_bulk = getenv("DDPMA_CHUNK") ? atoi(getenv("DDPMA_CHUNK")) : 8;
+  A.tmap = p->d_tmap;
   static unsigned long long* d_probe = nullptr;
   const char* pe = getenv("DDPMA_PROBE");
   if (pe) {
@@ -1193,6 +1196,7 @@ extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   if (p->h_act) cudaFreeHost(p->h_act);
   cudaFree(p->d_ndone);
   cudaFree(p->d_trace);
+  cudaFree(p->d_tmap);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->st) cudaStreamDestroy(p->st);
   delete p;
@@ -1473,6 +1477,48 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
         return fail(ce, "trace");
     }
     p->win_blocks = window_blocks(p->dim, P.pow2);
+    if (p->dim == 2 && getenv("DDPMA_NO_TMA") == nullptr) {
+      // one 2D tensor map per (subdomain, field, box): halo box 36 x (IR2+2) at
+      // (c0-2, r0-1), centre box 32 x IR2; out-of-box elements are zero-filled
+      typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+      void* fnp = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) ==
+              cudaSuccess && fnp) {
+        EncodeFn enc = (EncodeFn)fnp;
+        double* fields[TF_N] = {p->F.y[0], p->F.y[1], p->F.f[0], p->F.f[1],
+                                p->F.d[0], p->F.d[1], p->F.d[2], p->F.mr};
+        std::vector<CUtensorMap> maps((size_t)nl * TF_N * 2);
+        bool ok = true;
+        for (int l = 0; l < nl && ok; ++l) {
+          const SubGeo& g = p->geo[l];
+          const cuuint64_t gdim[2] = {(cuuint64_t)g.n[1], (cuuint64_t)g.n[0]};
+          const cuuint64_t gstr[1] = {(cuuint64_t)g.pitch * 8};
+          const cuuint32_t estr[2] = {1, 1};
+          for (int f = 0; f < TF_N && ok; ++f) {
+            for (int kind = 0; kind < 2; ++kind) {
+              const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)(TX + 4) : (cuuint32_t)TX,
+                                         kind == 0 ? (cuuint32_t)(IR2 + 2) : (cuuint32_t)IR2};
+              CUresult r = enc(&maps[((size_t)l * TF_N + f) * 2 + kind], CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                               2, fields[f] + g.off, gdim, gstr, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+              if (r != CUDA_SUCCESS) ok = false;
+            }
+          }
+        }
+        if (ok) {
+          if ((ce = cudaMalloc(&p->d_tmap, sizeof(CUtensorMap) * maps.size())) != cudaSuccess)
+            return fail(ce, "tmap");
+          if ((ce = cudaMemcpy(p->d_tmap, maps.data(), sizeof(CUtensorMap) * maps.size(),
+                               cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail(ce, "tmap copy");
+        }
+      }
+    }
     p->host_ctl = getenv("DDPMA_HOST_CONTROLLER") != nullptr;
   }
   p->stage_cap = 1 << 20;
