@@ -16,7 +16,7 @@ from .errors import (ConfigurationError, DdmeshError, InvalidMonitorError,
                      StiffnessError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libddpma.so")
+LIB_PATH = os.environ.get("DDPMA_LIB") or os.path.join(_HERE, "libddpma.so")
 
 OK, ERR_CONFIG, ERR_INVALID_MONITOR, ERR_STIFFNESS, ERR_CUDA, ERR_STATE, ERR_VALUE, \
     ERR_OVERFLOW = range(8)

@@ -25,21 +25,21 @@
 namespace ddpma {
 namespace dev {
 
-__host__ __device__ __forceinline__ double fastlog(double x) {
+// `tab` = the {inv_k, T_hi, T_lo} table (kLogTabD in global memory, or a
+// shared-memory copy of it in the window kernel).
+__host__ __device__ __forceinline__ double fastlog_t(double x, const double (*tab)[3]) {
 #ifdef __CUDA_ARCH__
-  const double(*tab)[3] = kLogTabD;
 #define DDPMA_FMA(a, b, c) __fma_rn((a), (b), (c))
 #else
-  const double(*tab)[3] = kLogTabH;
 #define DDPMA_FMA(a, b, c) std::fma((a), (b), (c))
 #endif
-  if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
-  if (x == INFINITY) return x;
   long long bits;
   memcpy(&bits, &x, 8);
   int e = (int)(bits >> 52) - 1023;
-  if (e == -1023) {   // subnormal: scale into the normal range
-    const double xs = x * 0x1p54;
+  if (!(x >= 0x1p-1022 && x < INFINITY)) {   // one test for the common (positive normal) case
+    if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
+    if (x == INFINITY) return x;
+    const double xs = x * 0x1p54;   // subnormal: scale into the normal range
     memcpy(&bits, &xs, 8);
     e = (int)(bits >> 52) - 1023 - 54;
   }
@@ -72,6 +72,14 @@ __host__ __device__ __forceinline__ double fastlog(double x) {
   const double e2 = (s - (a - bv)) + (r - bv);
   return a + (e2 + lo);
 #undef DDPMA_FMA
+}
+
+__host__ __device__ __forceinline__ double fastlog(double x) {
+#ifdef __CUDA_ARCH__
+  return fastlog_t(x, kLogTabD);
+#else
+  return fastlog_t(x, kLogTabH);
+#endif
 }
 
 }  // namespace dev

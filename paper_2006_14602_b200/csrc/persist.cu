@@ -28,6 +28,10 @@
 #include "ddpma_internal.h"
 #include "stencil.cuh"
 
+#ifndef DDPMA_MINB2
+#define DDPMA_MINB2 4   // resident CTAs per SM of the 2D window kernel (register cap)
+#endif
+
 namespace ddpma {
 
 namespace {
@@ -41,6 +45,10 @@ enum { R_START = 0, R_ACCEPT, R_REJECT };
 constexpr double kSqrtEps = 1.4901161193847656e-08;   // np.sqrt(np.finfo(float).eps)
 constexpr double kStab = 0.653;                       // integrate.py:36
 constexpr double kMinStep = 1e-14;                    // integrate.py:37
+
+// Shared-memory copy of the log table (filled at the start of k_windowP;
+// the table lookups are the fp64 log's only memory accesses).
+__shared__ double s_logtab[97][3];
 
 // coherent (L2) loads of mutable data
 __device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
@@ -909,6 +917,12 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(unsigned long long* m) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(m)) : "memory");
 }
+__device__ __forceinline__ void mbar_init_n(unsigned long long* m, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(m)) : "memory");
+}
 __device__ __forceinline__ void mbar_expect(unsigned long long* m, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
                "r"(bytes)
@@ -1003,7 +1017,7 @@ struct TileAcc2 {
 };
 
 template <bool P2, int MODE, int YM>
-__device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+__device__ __noinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
                                          int r0, const Stage2& st, Acc& acc, double* psum_item) {
   constexpr int R = IR2 / TY;
   // how Y is formed from global memory (outside the tile) for this mode
@@ -1061,14 +1075,20 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
       const double h01 = dv<P2>(gp - gm, A.P.ax[0].twoh, A.P.ax[0].itwoh);
       det[q] = h00 * h11 - h01 * h01;
     }
-    // phase 2: generic face formulas (rare)
+    // phase 2: generic face formulas (rare).  Dirichlet (interface-face)
+    // nodes need no determinant: F = 0 there and they never raise the flag.
+    unsigned dirm = 0u;
     if (edge) {
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (edge & (1u << q)) {
           const int i0 = r0 + threadIdx.y + q * TY;
-          det[q] = hdet<2, P2>(A.P, g, i0, i1, 0,
-                               TileAcc2<YM, YMG>{&st, r0, c0, GAcc<2, YMG>{&g, yb, ap, t.c}});
+          if (dirichlet<2>(g, i0, i1, 0)) {
+            dirm |= 1u << q;
+          } else {
+            det[q] = hdet<2, P2>(A.P, g, i0, i1, 0,
+                                 TileAcc2<YM, YMG>{&st, r0, c0, GAcc<2, YMG>{&g, yb, ap, t.c}});
+          }
         }
       }
     }
@@ -1077,10 +1097,9 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int lr = threadIdx.y + q * TY;
-      const int i0 = r0 + lr;
-      const bool dir = ((edge >> q) & 1u) && dirichlet<2>(g, i0, i1, 0);   // faces only
+      const bool dir = (dirm >> q) & 1u;
       const int pc = lr * TX + threadIdx.x;
-      F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor, A.P.rguard);
+      F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor, A.P.rguard, s_logtab);
       acc.flag |= ((valid >> q) & 1u) && det[q] <= A.P.floor && !dir ? 1u : 0u;
     }
     // phase 4: epilogues
@@ -1126,6 +1145,118 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
       }
     }
     *psum_item = ps;
+  }
+}
+
+// Face-node determinant (generic one-sided formulas, hdet<2>), out of line so
+// its register needs do not constrain the hot path.
+template <bool P2, int YM>
+__device__ __noinline__ double hdet_face(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
+                                         int i1, int r0, int c0, const Stage2& st,
+                                         const double* yb, const double* ap) {
+  return hdet<2, P2>(A.P, g, i0, i1, 0,
+                     TileAcc2<YM, YM>{&st, r0, c0, GAcc<2, YM>{&g, yb, ap, t.c}});
+}
+
+// Fused RHS + epilogue of one 2D item for the modes without partial sums
+// (F0, EULER, STAGE2/3/N, FINAL).  Thread (tx, ty) owns the two consecutive
+// rows 2ty and 2ty+1 of column tx, so the 3x4 Y neighbourhood is loaded once
+// for both nodes.  Every node first takes compute2's branch-free interior
+// formula (same expressions, same order: bitwise identical); with EDGE (the
+// item touches a box face or extends past the box) face nodes are then
+// patched exactly as compute2 does: Dirichlet (interface) nodes get F = 0 and
+// no determinant, physical-face nodes the one-sided formulas of hdet<2>, and
+// nodes past the box are skipped.
+template <bool P2, int MODE, int YM, bool EDGE>
+__device__ __forceinline__ void compute2_int(const WinArgs& A, const SubGeo& g, const Act& t,
+                                             long long kb, long long pitch, int r0, int c0,
+                                             int n0, int n1, const Stage2& st, Acc& acc) {
+  const int tx = threadIdx.x, lr = 2 * threadIdx.y;
+  const int p = (lr + 1) * TW2 + tx + 2;       // tile index of node (lr, tx)
+  const int par = (r0 + c0 + lr + tx) & 1;     // (i0 + i1) & 1 of node (lr, tx)
+  double w[4], c[4], e[4];                     // tile rows lr-1 .. lr+2, columns tx-1..tx+1
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int b = p + (r - 1) * TW2;
+    const int pr = par ^ ((r + 1) & 1);        // parity of (lr + r - 1, tx)
+    w[r] = yat<YM>(st, b - 1, t.c, pr ^ 1);
+    c[r] = yat<YM>(st, b, t.c, pr);
+    e[r] = yat<YM>(st, b + 1, t.c, pr ^ 1);
+  }
+  const double ihh0 = A.P.ax[0].ihh, hh0 = A.P.ax[0].hh, ihh1 = A.P.ax[1].ihh, hh1 = A.P.ax[1].hh;
+  const double it0 = A.P.ax[0].itwoh, tw0 = A.P.ax[0].twoh, it1 = A.P.ax[1].itwoh,
+               tw1 = A.P.ax[1].twoh;
+  double gd[4];                                // (e - w)/2h1 per row: gm of row r+1, gp of r-1
+#pragma unroll
+  for (int r = 0; r < 4; ++r) gd[r] = dv<P2>(e[r] - w[r], tw1, it1);
+  double F[2], det[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const double yc = c[q + 1];
+    const double h00 = dv<P2>((c[q + 2] - 2.0 * yc) + c[q], hh0, ihh0);
+    const double h11 = dv<P2>((e[q + 1] - 2.0 * yc) + w[q + 1], hh1, ihh1);
+    const double h01 = dv<P2>(gd[q + 2] - gd[q], tw0, it0);
+    det[q] = h00 * h11 - h01 * h01;
+  }
+  unsigned valid = 3u, dirm = 0u;
+  if constexpr (EDGE) {
+    const double* yb = A.F.y[t.yi];
+    const double* ap = nullptr;
+    if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
+    if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
+    if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
+    const int i1 = c0 + tx;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i0 = r0 + lr + q;
+      if (!(i0 < n0 && i1 < n1)) {
+        valid &= ~(1u << q);
+      } else if (i0 == 0 || i0 == n0 - 1 || i1 == 0 || i1 == n1 - 1) {
+        if (dirichlet<2>(g, i0, i1, 0)) dirm |= 1u << q;
+        else det[q] = hdet_face<P2, YM>(A, g, t, i0, i1, r0, c0, st, yb, ap);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int pc = (lr + q) * TX + tx;
+    const bool dir = (dirm >> q) & 1u;
+    F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor, A.P.rguard, s_logtab);
+    acc.flag |= ((valid >> q) & 1u) && !dir && det[q] <= A.P.floor ? 1u : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (EDGE && !((valid >> q) & 1u)) continue;
+    const int pq = p + q * TW2;
+    const int pc = (lr + q) * TX + tx;
+    const long long k = kb + (long long)(lr + q) * pitch;
+    if constexpr (MODE == M_F0) {
+      A.F.f[t.fi][k] = F[q];
+    } else if constexpr (MODE == M_EULER) {
+      A.F.y[1 - t.yi][k] = st.ys[pq] + t.c * F[q];
+    } else if constexpr (MODE == M_STAGE2) {
+      const double f0 = st.as[pq];
+      const double d1 = t.c * f0;
+      A.F.d[2][k] = ((t.mu * d1 + t.nu * 0.0) + t.hmut * F[q]) + t.hgt * f0;
+    } else if constexpr (MODE == M_STAGE3) {
+      const double f0 = st.cf[pc];
+      const double d1 = t.c * f0;
+      A.F.d[0][k] = ((t.mu * st.as[pq] + t.nu * d1) + t.hmut * F[q]) + t.hgt * f0;
+    } else if constexpr (MODE == M_STAGEN) {
+      const double f0 = st.cf[pc];
+      A.F.d[t.j % 3][k] = ((t.mu * st.as[pq] + t.nu * st.cd[pc]) + t.hmut * F[q]) + t.hgt * f0;
+    } else if constexpr (MODE == M_FINAL) {
+      const double ds = st.as[pq], yv = st.ys[pq], f0 = st.cf[pc];
+      const double yn = yv + ds;
+      A.F.f[1 - t.fi][k] = F[q];
+      A.F.y[1 - t.yi][k] = yn;
+      const double err = -0.8 * ds + t.h04 * (f0 + F[q]);
+      const double ay = fabs(yv), an = fabs(yn);
+      const double mx = (ay >= an || isnan(ay)) ? ay : an;
+      const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
+      if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
+      else acc.nonfin = 1;
+    }
   }
 }
 
@@ -1242,25 +1373,40 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
                        Stage2* stage, Acc& acc, double* sh_sum, unsigned long long* mbar,
                        unsigned& phases) {
   constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
+  // box geometry in registers (the geo table is immutable during the kernel)
+  const int n0 = __ldg(&g.n[0]), n1 = __ldg(&g.n[1]), items_x = __ldg(&g.items_x);
+  const long long pitch = __ldg(&g.pitch), goff = __ldg(&g.off);
   // item -> (column, row) tile origin, decoded once per chunk then stepped
-  int ix = it0 % g.items_x, iy = it0 / g.items_x;
+  int ix = it0 % items_x, iy = it0 / items_x;
   int nx = ix + 1, ny = iy;
-  if (nx == g.items_x) {
+  if (nx == items_x) {
     nx = 0;
     ++ny;
   }
   const bool tma = A.tmap != nullptr;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  // TMA pipeline: mbar[b] = "buffer b full" (1 arrival + tx bytes), mbar[2+b]
+  // = "buffer b consumed" (one arrival per warp).  phases: bits 0-1 full
+  // parity, 2-3 consumed parity, 4-5 buffer used before.  The issuing thread
+  // waits for the previous use of a buffer to be consumed by every warp, so
+  // warps never meet at a CTA barrier between items.
+  auto issue = [&](int b, int cx, int cy) {
+    if ((phases >> (4 + b)) & 1u) {
+      mbar_wait(&mbar[2 + b], (phases >> (2 + b)) & 1u);
+      phases ^= 1u << (2 + b);
+    }
+    phases |= 1u << (4 + b);
+    issue2_tma<MODE, YM>(A, t.sub, t, cx * TX, cy * IR2, stage[b], &mbar[b]);
+  };
   if (tma) {
-    if (lead) issue2_tma<MODE, YM>(A, t.sub, t, ix * TX, iy * IR2, stage[0], &mbar[0]);
+    if (lead) issue(0, ix, iy);
   } else {
     issue2<MODE, YM>(A, g, t, ix * TX, iy * IR2, stage[0]);
   }
   for (int i = 0; i < nit; ++i) {
     const int s = i & 1;
     if (tma) {
-      if (i + 1 < nit && lead)
-        issue2_tma<MODE, YM>(A, t.sub, t, nx * TX, ny * IR2, stage[s ^ 1], &mbar[s ^ 1]);
+      if (i + 1 < nit && lead) issue(s ^ 1, nx, ny);
       mbar_wait(&mbar[s], (phases >> s) & 1u);
       phases ^= 1u << s;
     } else {
@@ -1272,32 +1418,31 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
       }
       __syncthreads();
     }
-    if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
-      // Y = y + d (or y + c*f0) once per tile point instead of 9x per node;
-      // the centre of the a tile (d_{j-1} / f0) stays intact for the epilogue
-      Stage2& sg = stage[i & 1];
-      const int tid = threadIdx.y * TX + threadIdx.x;
-      for (int e = tid; e < TH2 * TW2; e += NT) {
-        if constexpr (YM == YM_ADD) sg.ys[e] = sg.ys[e] + sg.as[e];
-        else sg.ys[e] = sg.ys[e] + t.c * sg.as[e];
-      }
-      __syncthreads();
-    }
     double ps = 0.0;
-    constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
-    compute2<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, ix * TX, iy * IR2, stage[i & 1], acc,
-                                                 &ps);
+    const int c0 = ix * TX, r0 = iy * IR2;
+    const long long kb = goff + (long long)r0 * pitch + c0 + threadIdx.x;
+    if constexpr (SUMS) {
+      compute2<P2, MODE, YM>(A, g, t, c0, r0, stage[s], acc, &ps);
+    } else if (r0 >= 1 && r0 + IR2 <= n0 - 1 && c0 >= 1 && c0 + TX <= n1 - 1) {
+      compute2_int<P2, MODE, YM, false>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[s], acc);
+    } else {
+      compute2_int<P2, MODE, YM, true>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[s], acc);
+    }
     ix = nx;
     iy = ny;
-    if (++nx == g.items_x) {
+    if (++nx == items_x) {
       nx = 0;
       ++ny;
+    }
+    if (tma) {
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&mbar[2 + s]);   // this warp is done with buffer s
     }
     if constexpr (SUMS) {
       const double s = block_sum(ps, sh_sum);   // per-item partial: deterministic
       if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, s);
     } else {
-      __syncthreads();   // the stage buffer is refilled by the next iteration's issue
+      if (!tma) __syncthreads();   // the stage buffer is refilled by the next iteration's issue
     }
   }
 }
@@ -1479,7 +1624,7 @@ __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, cons
                           TileAcc3<YM, YMG>{&st, z0, r0, c0, GAcc<3, YMG>{&g, yb, ap, t.c}});
       }
       const bool dir = !interior && dirichlet<3>(g, i0, i1, i2);
-      const double F = dir ? 0.0 : logequi(st.cm[pc], det, A.P.guard, A.P.floor, A.P.rguard);
+      const double F = dir ? 0.0 : logequi(st.cm[pc], det, A.P.guard, A.P.floor, A.P.rguard, s_logtab);
       acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
       if constexpr (MODE == M_F0) {
         A.F.f[t.fi][k] = F;
@@ -1582,18 +1727,22 @@ __device__ void dispatch_chunk3(const WinArgs& A, const SubGeo& g, const Act& t,
 }
 
 template <int DIM, bool P2>
-__global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 3) k_windowP(const WinArgs A) {
+__global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(const WinArgs A) {
   using Stage = typename std::conditional<DIM == 2, Stage2, Stage3>::type;
   extern __shared__ __align__(128) unsigned char dsm[];
   Stage* stage = reinterpret_cast<Stage*>(
       dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
-  __shared__ __align__(8) unsigned long long s_mbar[2];
+  __shared__ __align__(8) unsigned long long s_mbar[4];
   unsigned phases = 0u;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     mbar_init(&s_mbar[0]);
     mbar_init(&s_mbar[1]);
+    mbar_init_n(&s_mbar[2], NT / 32);
+    mbar_init_n(&s_mbar[3], NT / 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  for (int i = threadIdx.y * TX + threadIdx.x; i < 97 * 3; i += NT)
+    (&s_logtab[0][0])[i] = (&kLogTabD[0][0])[i];
   __syncthreads();
   __shared__ double sh_sum[NT / 32];
   __shared__ unsigned long long sh_max[NT / 32];
