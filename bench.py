@@ -310,7 +310,10 @@ def run_gpu(args):
                if traffic_per_node else None)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": "k_eval<2,pow2> fused RHS+RKC2 stage (48 B/node-update at stage j>=4)",
+                "kernel": ("k_windowW<pow2> persistent warp-specialised window kernel: fused "
+                           "RHS + RKC2 stage / final / f0 / power actions (48 B/node-update at "
+                           "stage j>=4)" if os.environ.get("DDPMA_WS", "0") != "0" else
+                           "k_windowP<2,pow2> persistent window kernel"),
                 "algo_bytes_per_launch": prof["bytes"][k] / max(1, int(prof["launches"][k])),
                 "avg_launch_ms": prof["ms"][k] / max(1, int(prof["launches"][k])),
                 "share_of_step": round(share, 4), "peak_source": peak_src}

@@ -202,7 +202,8 @@ struct WinArgs {
   int trace_cap;
   unsigned long long* probe;   // debug: [cap][4] = publish, first claim, last done, decided
   int probe_sub, probe_cap;
-  int chunk_bulk;            // items per claim while >= 16 subdomains are active
+  int chunk_bulk;            // items per claim while >= tail_n subdomains are active
+  int chunk_tail, tail_n;    // items per claim below that (the tail's critical path)
   const void* tmap;          // 2D: CUtensorMap[nlocal][8 fields][2 boxes] (TMA tile loads), or null
 };
 

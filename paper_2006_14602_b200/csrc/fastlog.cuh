@@ -25,6 +25,14 @@
 namespace ddpma {
 namespace dev {
 
+// log1p Taylor coefficients 1/7, -1/6, 1/5, 1/3 and ln2 = hi + lo
+#define DDPMA_LOGPOLY \
+  {0x1.2492492492492p-3, -0x1.5555555555555p-3, 0.2, 0x1.5555555555555p-2, kLn2Hi, kLn2Lo}
+#ifdef __CUDACC__
+__constant__ double kLogPolyD[6] = DDPMA_LOGPOLY;
+#endif
+static const double kLogPolyH[6] = DDPMA_LOGPOLY;
+
 // `tab` = the {inv_k, T_hi, T_lo} table (kLogTabD in global memory, or a
 // shared-memory copy of it in the window kernel).
 __host__ __device__ __forceinline__ double fastlog_t(double x, const double (*tab)[3]) {
@@ -53,20 +61,25 @@ __host__ __device__ __forceinline__ double fastlog_t(double x, const double (*ta
   const double pm = m * t[0];                   // m*inv = pm + plo exactly
   const double plo = DDPMA_FMA(m, t[0], -pm);
   const double r = pm - 1.0;                    // exact (Sterbenz: pm in [1-2^-7.5, 1+2^-7.5])
+#ifdef __CUDA_ARCH__
+  const double* C = kLogPolyD;   // constant bank: DFMA takes c[][] operands directly
+#else
+  const double* C = kLogPolyH;
+#endif
   double q = -0.125;
-  q = DDPMA_FMA(q, r, 0x1.2492492492492p-3);    // 1/7
-  q = DDPMA_FMA(q, r, -0x1.5555555555555p-3);   // -1/6
-  q = DDPMA_FMA(q, r, 0.2);
+  q = DDPMA_FMA(q, r, C[0]);    // 1/7
+  q = DDPMA_FMA(q, r, C[1]);    // -1/6
+  q = DDPMA_FMA(q, r, C[2]);    // 0.2
   q = DDPMA_FMA(q, r, -0.25);
-  q = DDPMA_FMA(q, r, 0x1.5555555555555p-2);    // 1/3
+  q = DDPMA_FMA(q, r, C[3]);    // 1/3
   q = DDPMA_FMA(q, r, -0.5);
   const double r2 = r * r;
   const double ed = (double)e;
-  const double big = ed * kLn2Hi;               // exact
+  const double big = ed * C[4];                 // ed * ln2_hi: exact
   const double s = big + t[1];
   const double err = (big - s) + t[1];          // Fast2Sum (|big| >= |T| or big = 0)
   // log1p(r + plo) = log1p(r) + plo/(1+r) + O(plo^2): plo/(1+r) ~ plo - plo*r
-  const double lo = DDPMA_FMA(r2, q, (DDPMA_FMA(ed, kLn2Lo, t[2]) + err) + DDPMA_FMA(-plo, r, plo));
+  const double lo = DDPMA_FMA(r2, q, (DDPMA_FMA(ed, C[5], t[2]) + err) + DDPMA_FMA(-plo, r, plo));
   const double a = s + r;                       // TwoSum(s, r): r and T partially cancel near 1
   const double bv = a - s;
   const double e2 = (s - (a - bv)) + (r - bv);

@@ -931,7 +931,7 @@ __device__ __forceinline__ void mbar_expect(unsigned long long* m, unsigned byte
 __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
       "r"(phase)
       : "memory");
@@ -1017,7 +1017,7 @@ struct TileAcc2 {
 };
 
 template <bool P2, int MODE, int YM>
-__device__ __noinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
+__device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
                                          int r0, const Stage2& st, Acc& acc, double* psum_item) {
   constexpr int R = IR2 / TY;
   // how Y is formed from global memory (outside the tile) for this mode
@@ -1148,10 +1148,9 @@ __device__ __noinline__ void compute2(const WinArgs& A, const SubGeo& g, const A
   }
 }
 
-// Face-node determinant (generic one-sided formulas, hdet<2>), out of line so
-// its register needs do not constrain the hot path.
+// Face-node determinant (generic one-sided formulas, hdet<2>).
 template <bool P2, int YM>
-__device__ __noinline__ double hdet_face(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
+__device__ __forceinline__ double hdet_face(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
                                          int i1, int r0, int c0, const Stage2& st,
                                          const double* yb, const double* ap) {
   return hdet<2, P2>(A.P, g, i0, i1, 0,
@@ -1755,7 +1754,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
     if (threadIdx.y == 0) {
       // chunk of 4 items while many subdomains are active, 1 on the tail
       const unsigned nd = *(volatile unsigned*)A.n_done;
-      const int chunk = (A.nact - (int)nd) >= 16 ? A.chunk_bulk : 1;
+      const int chunk = (A.nact - (int)nd) >= A.tail_n ? A.chunk_bulk : A.chunk_tail;
       int got, it0, nit;
       claim(A, chunk, got, it0, nit);
       if (threadIdx.x == 0) {
@@ -1854,13 +1853,290 @@ __global__ void k_window_begin(const WinArgs A) {
   d_publish(A, c, gc);
 }
 
+// ============================================================================
+// Warp-specialised 2D window kernel (k_windowW): 8 consumer warps + 1
+// producer warp per CTA.
+//
+// The producer warp claims chunks (claim-ahead: the next chunk is claimed
+// while the consumers still work on the current one), publishes each chunk's
+// action through a 2-slot mailbox (mbarriers cfull / cempty) and streams every
+// item's tiles into an NS-deep ring of shared-memory stages with TMA (full[b]:
+// transaction bytes; empty[b]: one arrival per consumer warp).  Consumers
+// never meet the producer at a barrier; among themselves they synchronise
+// only at chunk ends (named barrier 1) for the flag / error-ratio reductions
+// and the completion accounting.  The per-item arithmetic is compute2_int /
+// compute2 (bitwise identical to the other window kernels).
+// ============================================================================
+
+constexpr int NS2 = 3;                 // ring depth (stages) of k_windowW
+constexpr int NTW = NT + 32;           // threads per CTA of k_windowW
+
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+__device__ __forceinline__ int cbar_or(int p) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred pi, po;\n setp.ne.s32 pi, %1, 0;\n"
+      " bar.red.or.pred po, 1, 256, pi;\n selp.s32 %0, 1, 0, po;\n}\n"
+      : "=r"(r)
+      : "r"(p)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ double csum(double v, double* sh) {   // block_sum over consumers
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if (threadIdx.x == 0) sh[threadIdx.y] = v;
+  cbar();
+  double tot = 0.0;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    tot = sh[0];
+    for (int w = 1; w < NT / 32; ++w) tot += sh[w];
+  }
+  cbar();
+  return tot;
+}
+__device__ __forceinline__ unsigned long long cmax(unsigned long long v, unsigned long long* sh) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_down_sync(0xffffffffu, v, off);
+    v = o > v ? o : v;
+  }
+  if (threadIdx.x == 0) sh[threadIdx.y] = v;
+  cbar();
+  unsigned long long m = 0;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    m = sh[0];
+    for (int w = 1; w < NT / 32; ++w) m = sh[w] > m ? sh[w] : m;
+  }
+  cbar();
+  return m;
+}
+
+// Producer side: the TMA copies of one item for a runtime mode.
+__device__ __forceinline__ void issue_any2(const WinArgs& A, const Act& t, int c0, int r0,
+                                           Stage2& st, unsigned long long* mb) {
+  switch (t.mode) {
+    case M_F0: issue2_tma<M_F0, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_EULER: issue2_tma<M_EULER, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGE2: issue2_tma<M_STAGE2, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGE3: issue2_tma<M_STAGE3, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGEN: issue2_tma<M_STAGEN, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_FINAL: issue2_tma<M_FINAL, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_POWER: issue2_tma<M_POWER, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_POWER_SEED: issue2_tma<M_POWER_SEED, YM_SEED>(A, t.sub, t, c0, r0, st, mb); break;
+    default: issue2_tma<M_NORM, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+  }
+}
+
+// Consumer side of one chunk: n = ring position (items consumed so far).
+template <bool P2, int MODE, int YM>
+__device__ void cchunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
+                        Stage2* stage, Acc& acc, double* sh_sum, unsigned long long* full,
+                        unsigned long long* empty, unsigned& n) {
+  constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
+  const int n0 = __ldg(&g.n[0]), n1 = __ldg(&g.n[1]), items_x = __ldg(&g.items_x);
+  const long long pitch = __ldg(&g.pitch), goff = __ldg(&g.off);
+  int ix = it0 % items_x, iy = it0 / items_x;
+  for (int i = 0; i < nit; ++i, ++n) {
+    const unsigned b = n % NS2, u = n / NS2;
+    mbar_wait(&full[b], u & 1u);
+    double ps = 0.0;
+    const int c0 = ix * TX, r0 = iy * IR2;
+    const long long kb = goff + (long long)r0 * pitch + c0 + threadIdx.x;
+    if constexpr (SUMS) {
+      compute2<P2, MODE, YM>(A, g, t, c0, r0, stage[b], acc, &ps);
+    } else if (r0 >= 1 && r0 + IR2 <= n0 - 1 && c0 >= 1 && c0 + TX <= n1 - 1) {
+      compute2_int<P2, MODE, YM, false>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[b], acc);
+    } else {
+      compute2_int<P2, MODE, YM, true>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[b], acc);
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(&empty[b]);   // this warp is done with stage b
+    if (++ix == items_x) {
+      ix = 0;
+      ++iy;
+    }
+    if constexpr (SUMS) {
+      const double sv = csum(ps, sh_sum);   // per-item partial: deterministic
+      if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, sv);
+    }
+  }
+}
+
+template <bool P2>
+__device__ void dispatch_cchunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
+                                 int nit, Stage2* st, Acc& acc, double* sh,
+                                 unsigned long long* fu, unsigned long long* em, unsigned& n) {
+  switch (t.mode) {
+    case M_F0: cchunk2<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_EULER: cchunk2<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_STAGE2: cchunk2<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_STAGE3: cchunk2<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_STAGEN: cchunk2<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_FINAL: cchunk2<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_POWER: cchunk2<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    case M_POWER_SEED:
+      cchunk2<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh, fu, em, n);
+      break;
+    case M_NORM: cchunk2<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
+    default: break;
+  }
+}
+
+struct ChunkSlot {
+  Act t;
+  int it0, nit, exit, pad;
+};
+
+template <bool P2>
+__global__ void __launch_bounds__(NTW, 3) k_windowW(const WinArgs A) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Stage2* stage = reinterpret_cast<Stage2*>(
+      dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
+  __shared__ __align__(8) unsigned long long s_full[NS2], s_empty[NS2], s_cfull[2], s_cempty[2];
+  __shared__ ChunkSlot s_cs[2];
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_max[NT / 32];
+  __shared__ DevCtl s_ctl;
+  __shared__ int s_last;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    for (int b = 0; b < NS2; ++b) {
+      mbar_init(&s_full[b]);
+      mbar_init_n(&s_empty[b], NT / 32);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&s_cfull[k]);
+      mbar_init(&s_cempty[k]);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = threadIdx.y * TX + threadIdx.x; i < 97 * 3; i += NTW)
+    (&s_logtab[0][0])[i] = (&kLogTabD[0][0])[i];
+  __syncthreads();
+
+  if (threadIdx.y == TY) {
+    // ---------------------------------------------------------- producer
+    const int lane = threadIdx.x;
+    unsigned n = 0;       // items issued
+    int k = 0;            // chunks published
+    unsigned backoff = 32;
+    while (true) {
+      const int slot = k & 1;
+      if (k >= 2) mbar_wait(&s_cempty[slot], ((k >> 1) - 1) & 1);
+      const unsigned nd = *(volatile unsigned*)A.n_done;
+      const int chunk = (A.nact - (int)nd) >= A.tail_n ? A.chunk_bulk : A.chunk_tail;
+      int got, it0, nit;
+      claim(A, chunk, got, it0, nit);
+      if (got < 0) {
+        if (*(volatile unsigned*)A.n_done >= (unsigned)A.nact) {
+          if (lane == 0) {
+            s_cs[slot].exit = 1;
+            mbar_arrive(&s_cfull[slot]);
+          }
+          break;
+        }
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? backoff * 2 : 256;
+        continue;
+      }
+      backoff = 32;
+      if (lane == 0) {
+        __threadfence();   // acquire: the action and the data of the previous action
+        const Act t = load_act(A, got);
+        s_cs[slot].t = t;
+        s_cs[slot].it0 = it0;
+        s_cs[slot].nit = nit;
+        s_cs[slot].exit = 0;
+        mbar_arrive(&s_cfull[slot]);
+        const int items_x = __ldg(&A.geo[got].items_x);
+        int ix = it0 % items_x, iy = it0 / items_x;
+        for (int i = 0; i < nit; ++i, ++n) {
+          const unsigned b = n % NS2, u = n / NS2;
+          if (u >= 1) mbar_wait(&s_empty[b], (u - 1) & 1u);
+          issue_any2(A, t, ix * TX, iy * IR2, stage[b], &s_full[b]);
+          if (++ix == items_x) {
+            ix = 0;
+            ++iy;
+          }
+        }
+      }
+      __syncwarp();
+      ++k;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  unsigned n = 0;
+  int k = 0;
+  while (true) {
+    const int slot = k & 1;
+    mbar_wait(&s_cfull[slot], (k >> 1) & 1);
+    const int ex = s_cs[slot].exit;
+    // the action stays in the mailbox slot (read from shared memory where
+    // used) until the chunk is complete; the slot is released at chunk end
+    const Act& t = s_cs[slot].t;
+    const int it0 = s_cs[slot].it0, nit = s_cs[slot].nit;
+    ++k;
+    if (ex) break;
+    const int l = t.sub;
+    const SubGeo& g = A.geo[l];
+    Acc acc{0u, 0u, 0.0, 0.0};
+    dispatch_cchunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_full, s_empty, n);
+    const int any = cbar_or(acc.flag);
+    const int anynf = cbar_or(acc.nonfin);
+    unsigned long long emax = 0ull;
+    if (t.mode == M_FINAL)
+      emax = cmax((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
+    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
+    if (tid == 0) {
+      DevCtl* gc = A.ctl + l;
+      unsigned bits = 0;
+      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
+      if (anynf) bits |= 4u;
+      if (bits) atomicOr(&gc->acc_flags, bits);
+      if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
+      __threadfence();
+      const unsigned d = atomicAdd(&gc->done, (unsigned)nit);
+      s_last = d + (unsigned)nit == (unsigned)g.nitems;
+    }
+    cbar();
+    if (s_last) {
+      __threadfence();
+      double sum = 0.0;
+      if (sums) {
+        double v = 0.0;
+        for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
+        sum = csum(v, sh_sum);
+      }
+      if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
+    }
+    cbar();
+    if (tid == 0) mbar_arrive(&s_cempty[slot]);   // mailbox slot free
+  }
+}
+
 }  // namespace
+
+// DDPMA_WS=1 selects the warp-specialised 2D kernel k_windowW (default: the
+// single-role k_windowP, measured faster on C3: 4 vs 3 resident CTAs per SM).
+static bool window_ws() {
+  static const int ws = getenv("DDPMA_WS") ? atoi(getenv("DDPMA_WS")) : 0;
+  return ws != 0;
+}
 
 int window_blocks(int dim, int pow2) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (dim == 2) {
+  if (dim == 2 && window_ws()) {
+    const int smem = NS2 * STAGE2_BYTES + 128;
+    cudaFuncSetAttribute(k_windowW<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_windowW<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowW<true>, NTW, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowW<false>, NTW, smem);
+  } else if (dim == 2) {
     const int smem = 2 * STAGE2_BYTES + 128;
     cudaFuncSetAttribute(k_windowP<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_windowP<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1887,7 +2163,12 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   void* args[] = {(void*)&a};
   void* fn;
   size_t smem = 0;
-  if (a.P.dim == 2) {
+  if (a.P.dim == 2 && window_ws() && a.tmap != nullptr) {
+    fn = a.P.pow2 ? (void*)k_windowW<true> : (void*)k_windowW<false>;
+    smem = NS2 * STAGE2_BYTES + 128;
+    cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(TX, TY + 1), args, smem, (cudaStream_t)stream);
+    return;
+  } else if (a.P.dim == 2) {
     fn = a.P.pow2 ? (void*)k_windowP<2, true> : (void*)k_windowP<2, false>;
     smem = 2 * STAGE2_BYTES + 128;
   } else {
