@@ -253,6 +253,21 @@ ddpma_status ddpma_rkc_step(ddpma_plan* plan, int sub_id, const double* y_host,
                             int s, double* d_host, double* fnew_host,
                             int* flagged, int* end_flagged);
 
+/* metrics.quality_measure (metrics.py:57-85) of a steady potential on the
+ * plan's box (a single-box plan of the grid): e_adp = |Omega_c| rho J per
+ * node into e_host (box-shaped, may be NULL) and report[0..4] = {e2, emax,
+ * node_mean, tangled (0/1), normaliser used}.  rho = raw(clamp(x)) /
+ * normalizer (MonitorField.eval_clamped), or with sample_on_mesh = 1 the
+ * transport-normalised nodal density raw / sum(w*raw*J) (mesh_density
+ * without smoothing). */
+ddpma_status ddpma_quality(ddpma_plan* plan, int sub_id, const double* psi_host,
+                           double normalizer, int sample_on_mesh, double* e_host,
+                           double* report);
+/* metrics.relative_errors (metrics.py:100-118): out = {e1, e2, einf} of two
+ * box-shaped fields on the plan's box. */
+ddpma_status ddpma_relative_errors(ddpma_plan* plan, int sub_id, const double* psi_dd_host,
+                                   const double* psi_sd_host, double* out);
+
 /* -------------------------------------------------------------- metrics --- */
 
 /* Counters since plan creation: node-updates (box nodes x RHS evaluations,

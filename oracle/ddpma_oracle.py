@@ -873,6 +873,35 @@ def solve_single(grid, mon, domain, cfg, initial=None, trace=None):
 
 # -------------------------------------------------------- BASELINE cfgs ----
 
+# ------------------------------------------------------------ metrics ----
+
+def quality_measure(psi, raw_fn, domain, normalizer, geom, sample_on_mesh=False):
+    """ddmesh/metrics.py:57-85 (no smoothing): -> (e_adp, e2, emax, node_mean,
+    tangled).  rho = raw(clamp(x)) / normalizer (monitor.py:66-68), or with
+    sample_on_mesh raw / sum(w raw J) (metrics.py:75-77, mesh_density
+    monitor.py:151-180 without smoothing)."""
+    coords, jac = mesh_of(psi, geom)
+    w = trap_weights(jac.shape, geom.spacing)
+    raw = raw_fn(clamp(coords, domain))
+    if sample_on_mesh:
+        rho = raw / float(np.sum(w * raw * jac))
+    else:
+        rho = raw / normalizer
+    e = geom.measure * rho * jac
+    e2 = float(np.sqrt(np.sum(w * e * e) / np.sum(w)))
+    return e, e2, float(np.abs(e).max()), float(e.mean()), bool((jac <= 0.0).any())
+
+
+def relative_errors(psi_dd, psi_sd, geom):
+    """ddmesh/metrics.py:100-118 -> (e1, e2, einf)."""
+    diff = np.abs(psi_sd - psi_dd)
+    ref = np.abs(psi_sd)
+    w = trap_weights(diff.shape, geom.spacing)
+    e1 = float(np.sum(w * diff) / np.sum(w * ref))
+    e2 = float(np.sqrt(np.sum(w * diff * diff) / np.sum(w * ref * ref)))
+    return e1, e2, float(diff.max() / ref.max())
+
+
 def baseline_case(name):
     """The five BASELINE.json configs as (grid, layout, overlap, monitor,
     domain, windows, transmission) — SURVEY §8(d) restatement."""

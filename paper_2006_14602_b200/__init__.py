@@ -18,6 +18,8 @@ from .monitor import (MixtureDensity, MonitorField, RingDensity, ShellDensity,
                       UniformDensity, density_monitor, seeded_mixture)
 from .schwarz import (PhysicalMesh, SolverConfig, SolveResult, WindowRecord,
                       residual, solve, solve_single_domain)
+from .metrics import (ErrorReport, QualityReport, quality_measure, relative_errors,
+                      restrict_to_grid)
 
 __version__ = "0.1.0"
 
@@ -31,4 +33,5 @@ __all__ = [
     "solve", "solve_single_domain", "residual",
     "DdmeshError", "ConfigurationError", "DomainError", "InvalidMonitorError",
     "MeshFileError", "StiffnessError",
+    "QualityReport", "ErrorReport", "quality_measure", "relative_errors", "restrict_to_grid",
 ]

@@ -90,6 +90,8 @@ SIGNATURES = {
     "ddpma_mesh": (C.c_int, [_P, C.c_int, _D, _D, _D]),
     "ddpma_raw_density": (C.c_int, [_P, C.c_int, _D, _D]),
     "ddpma_residual": (C.c_int, [_P, C.c_int, _D, _D, _D]),
+    "ddpma_quality": (C.c_int, [_P, C.c_int, _D, C.c_double, C.c_int, _D, _D]),
+    "ddpma_relative_errors": (C.c_int, [_P, C.c_int, _D, _D, _D]),
     "ddpma_rkc_step": (C.c_int, [_P, C.c_int, _D, _D, C.c_double, C.c_double, C.c_int,
                                  _D, _D, _I, _I]),
     "ddpma_counters": (C.c_int, [_P, _I64, _I64, _I64, _D]),

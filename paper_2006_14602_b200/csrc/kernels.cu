@@ -540,6 +540,166 @@ void launch_box_mesh(const KArgs& a, int nb, double* coords, double* jac, double
   }
 }
 
+// ------------------------------------------------------------- metrics ---
+// metrics.quality_measure (metrics.py:57-85) and relative_errors
+// (metrics.py:100-118) on one box (the plan's single box = the whole grid).
+// Per CTA fixed-order partials: QP_N doubles per block, reduced by one CTA in
+// block order (deterministic).
+
+// trapezoid weight of box node (i0,i1,i2): quadrature.weights (quadrature.py:16-21)
+template <int DIM>
+__device__ __forceinline__ double box_weight(const Prob& P, const SubGeo& g, int i0, int i1,
+                                             int i2) {
+  const int idx[3] = {i0, i1, i2};
+  double w = 1.0;
+#pragma unroll
+  for (int q = 0; q < DIM; ++q) {
+    const double wq = (idx[q] == 0 || idx[q] == g.n[q] - 1) ? P.ax[q].w_end : P.ax[q].w_in;
+    w = q == 0 ? wq : w * wq;
+  }
+  return w;
+}
+
+constexpr int QP_N = 6;
+
+// mode 0: z = sum (w*raw)*jac (sample_on_mesh normaliser, metrics.py:75-77)
+// mode 1: e = (|Omega| * (raw / norm)) * jac; partials
+//         {sum (w*e)*e, sum w, max|e| key, sum e, nonpositive jac count, NaN seen}
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT) k_quality(const KArgs a, int mode, double norm,
+                                                double* e_out, double* part) {
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_u[NT / 32];
+  const int b = blockIdx.x;
+  const Entry en = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[en.sub];
+  int i0, i1, i2;
+  const bool valid = tile_node<DIM>(g, b - en.tile_begin, i0, i1, i2);
+  double s0 = 0.0, s1 = 0.0, s3 = 0.0, tang = 0.0, nan = 0.0;
+  unsigned long long mk = 0ull;
+  if (valid) {
+    const YAcc<DIM, YM_PLAIN> Y{&g, a.F.y[en.yi], nullptr, 0.0};
+    double x[3];
+#pragma unroll
+    for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
+    const double jac = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
+    const double raw = mon_raw<DIM>(*a.mon, x);
+    const double w = box_weight<DIM>(a.P, g, i0, i1, i2);
+    if (mode == 0) {
+      s0 = (w * raw) * jac;
+    } else {
+      const double e = (a.P.measure * (raw / norm)) * jac;
+      const long long dk = DIM == 2 ? (long long)i0 * g.n[1] + i1
+                                    : ((long long)i0 * g.n[1] + i1) * g.n[2] + i2;
+      e_out[dk] = e;
+      s0 = (w * e) * e;
+      s1 = w;
+      s3 = e;
+      tang = jac <= 0.0 ? 1.0 : 0.0;
+      nan = isnan(e) ? 1.0 : 0.0;
+      mk = okey(fabs(e));
+    }
+  }
+  double v[5] = {s0, s1, s3, tang, nan};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const double r = block_sum(v[q], sh_sum);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[(long long)b * QP_N + q] = r;
+  }
+  const unsigned long long m = block_max_u64(mk, sh_u);
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    part[(long long)b * QP_N + 5] = __longlong_as_double((long long)m);
+}
+
+// relative_errors partials on dense box arrays: {sum w*diff, sum w*ref,
+// sum (w*diff)*diff, sum (w*ref)*ref, max diff key, max ref key}
+template <int DIM>
+__global__ void __launch_bounds__(NT) k_relerr(const KArgs a, const double* dd, const double* sd,
+                                               double* part) {
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_u[NT / 32];
+  const int b = blockIdx.x;
+  const Entry en = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[en.sub];
+  int i0, i1, i2;
+  const bool valid = tile_node<DIM>(g, b - en.tile_begin, i0, i1, i2);
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  unsigned long long kd = 0ull, kr = 0ull;
+  if (valid) {
+    const long long dk = DIM == 2 ? (long long)i0 * g.n[1] + i1
+                                  : ((long long)i0 * g.n[1] + i1) * g.n[2] + i2;
+    const double diff = fabs(sd[dk] - dd[dk]);   // np.abs(psi_sd - psi_dd)
+    const double ref = fabs(sd[dk]);
+    const double w = box_weight<DIM>(a.P, g, i0, i1, i2);
+    v[0] = w * diff;
+    v[1] = w * ref;
+    v[2] = (w * diff) * diff;
+    v[3] = (w * ref) * ref;
+    kd = okey(diff);
+    kr = okey(ref);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double r = block_sum(v[q], sh_sum);
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[(long long)b * QP_N + q] = r;
+  }
+  const unsigned long long m1 = block_max_u64(kd, sh_u);
+  const unsigned long long m2 = block_max_u64(kr, sh_u);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    part[(long long)b * QP_N + 4] = __longlong_as_double((long long)m1);
+    part[(long long)b * QP_N + 5] = __longlong_as_double((long long)m2);
+  }
+}
+
+__device__ __forceinline__ double unkey(unsigned long long k) {
+  const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// One CTA: columns 0..nsum-1 summed in block order, the rest max-reduced
+// (ordered keys), results in out[0..QP_N-1].
+__global__ void __launch_bounds__(32) k_qfinal(const double* part, int nb, int nsum, double* out) {
+  const int q = threadIdx.x;
+  if (q >= QP_N) return;
+  if (q < nsum) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[(long long)b * QP_N + q];
+    out[q] = s;
+  } else {
+    unsigned long long m = 0ull;
+    for (int b = 0; b < nb; ++b) {
+      const unsigned long long k = (unsigned long long)__double_as_longlong(part[(long long)b * QP_N + q]);
+      m = k > m ? k : m;
+    }
+    out[q] = unkey(m);
+  }
+}
+
+void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,
+                    double* out, void* stream) {
+  if (nb <= 0) return;
+  const dim3 blk(TX, TY);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.P.dim == 2) {
+    if (a.P.pow2) k_quality<2, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+    else k_quality<2, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+  } else {
+    if (a.P.pow2) k_quality<3, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+    else k_quality<3, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+  }
+  k_qfinal<<<1, 32, 0, st>>>(part, nb, 5, out);
+}
+
+void launch_relerr(const KArgs& a, int nb, const double* dd, const double* sd, double* part,
+                   double* out, void* stream) {
+  if (nb <= 0) return;
+  const dim3 blk(TX, TY);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.P.dim == 2) k_relerr<2><<<nb, blk, 0, st>>>(a, dd, sd, part);
+  else k_relerr<3><<<nb, blk, 0, st>>>(a, dd, sd, part);
+  k_qfinal<<<1, 32, 0, st>>>(part, nb, 4, out);
+}
+
 void launch_box_copy(const KArgs& a, int nb, const double* src, double* dst, int to_arena,
                      void* stream) {
   if (nb <= 0) return;

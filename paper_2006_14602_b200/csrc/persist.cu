@@ -931,7 +931,7 @@ __device__ __forceinline__ void mbar_expect(unsigned long long* m, unsigned byte
 __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
       "r"(phase)
       : "memory");

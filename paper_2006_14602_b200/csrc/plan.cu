@@ -2068,6 +2068,114 @@ extern "C" ddpma_status ddpma_residual(ddpma_plan* p, int sub_id, const double* 
   return DDPMA_OK;
 }
 
+// metrics kernels (kernels.cu)
+namespace ddpma {
+void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,
+                    double* out, void* stream);
+void launch_relerr(const KArgs& a, int nb, const double* dd, const double* sd, double* part,
+                   double* out, void* stream);
+}  // namespace ddpma
+
+extern "C" ddpma_status ddpma_quality(ddpma_plan* p, int sub_id, const double* psi_host,
+                                      double normalizer, int sample_on_mesh, double* e_host,
+                                      double* report) {
+  const int l = local_of_checked(p, sub_id);
+  if (l < 0) {
+    p->err = "subdomain is not local to this plan";
+    return DDPMA_ERR_STATE;
+  }
+  CK(p, cudaSetDevice(p->device));
+  p->ctl[l].yi = 0;
+  ddpma_status s;
+  if ((s = h2d_box(p, l, psi_host, p->F.y[0])) != DDPMA_OK) return s;
+  const SubGeo& g = p->geo[l];
+  void* d;
+  int nb;
+  if ((s = do_box_entry(p, l, &d, &nb)) != DDPMA_OK) return s;
+  double *de = nullptr, *dpart = nullptr, *dout = nullptr;
+  CK(p, cudaMalloc((void**)&de, sizeof(double) * g.nodes));
+  CK(p, cudaMalloc((void**)&dpart, sizeof(double) * 6 * (size_t)nb));
+  CK(p, cudaMalloc((void**)&dout, sizeof(double) * 12));
+  KArgs a = base_args(p);
+  a.ent = (Entry*)d;
+  a.nent = 1;
+  double h[6] = {0, 0, 0, 0, 0, 0};
+  double norm = normalizer;
+  if (sample_on_mesh) {   // rho = raw / sum(w * raw * jac) (metrics.py:75-77)
+    launch_quality(a, nb, 0, 1.0, de, dpart, dout + 6, p->st);
+    if ((s = check_launch(p, "quality z")) == DDPMA_OK &&
+        cudaMemcpyAsync(h, dout + 6, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)
+      s = DDPMA_ERR_CUDA;
+    if (s == DDPMA_OK) s = sync(p);
+    norm = h[0];
+  }
+  if (s == DDPMA_OK) {
+    launch_quality(a, nb, 1, norm, de, dpart, dout, p->st);
+    s = check_launch(p, "quality");
+  }
+  if (s == DDPMA_OK && cudaMemcpyAsync(h, dout, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)
+    s = DDPMA_ERR_CUDA;
+  if (s == DDPMA_OK && e_host &&
+      cudaMemcpyAsync(e_host, de, sizeof(double) * g.nodes, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)
+    s = DDPMA_ERR_CUDA;
+  if (s == DDPMA_OK) s = sync(p);
+  cudaFree(de);
+  cudaFree(dpart);
+  cudaFree(dout);
+  if (s != DDPMA_OK) return s;
+  // QualityReport (metrics.py:24-33): e2, emax, node_mean, tangled, normaliser used
+  report[0] = std::sqrt(h[0] / h[1]);
+  report[1] = h[5];
+  report[2] = h[2] / (double)g.nodes;
+  report[3] = h[3] > 0.0 ? 1.0 : 0.0;
+  report[4] = norm;
+  return DDPMA_OK;
+}
+
+extern "C" ddpma_status ddpma_relative_errors(ddpma_plan* p, int sub_id, const double* dd_host,
+                                              const double* sd_host, double* out) {
+  const int l = local_of_checked(p, sub_id);
+  if (l < 0) {
+    p->err = "subdomain is not local to this plan";
+    return DDPMA_ERR_STATE;
+  }
+  CK(p, cudaSetDevice(p->device));
+  const SubGeo& g = p->geo[l];
+  void* d;
+  int nb;
+  ddpma_status s;
+  if ((s = do_box_entry(p, l, &d, &nb)) != DDPMA_OK) return s;
+  double *ddd = nullptr, *dsd = nullptr, *dpart = nullptr, *dout = nullptr;
+  CK(p, cudaMalloc((void**)&ddd, sizeof(double) * g.nodes));
+  CK(p, cudaMalloc((void**)&dsd, sizeof(double) * g.nodes));
+  CK(p, cudaMalloc((void**)&dpart, sizeof(double) * 6 * (size_t)nb));
+  CK(p, cudaMalloc((void**)&dout, sizeof(double) * 6));
+  if (cudaMemcpyAsync(ddd, dd_host, sizeof(double) * g.nodes, cudaMemcpyHostToDevice, p->st) != cudaSuccess ||
+      cudaMemcpyAsync(dsd, sd_host, sizeof(double) * g.nodes, cudaMemcpyHostToDevice, p->st) != cudaSuccess)
+    s = DDPMA_ERR_CUDA;
+  KArgs a = base_args(p);
+  a.ent = (Entry*)d;
+  a.nent = 1;
+  double h[6] = {0, 0, 0, 0, 0, 0};
+  if (s == DDPMA_OK) {
+    launch_relerr(a, nb, ddd, dsd, dpart, dout, p->st);
+    s = check_launch(p, "relative_errors");
+  }
+  if (s == DDPMA_OK && cudaMemcpyAsync(h, dout, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)
+    s = DDPMA_ERR_CUDA;
+  if (s == DDPMA_OK) s = sync(p);
+  cudaFree(ddd);
+  cudaFree(dsd);
+  cudaFree(dpart);
+  cudaFree(dout);
+  if (s != DDPMA_OK) return s;
+  // ErrorReport (metrics.py:114-117)
+  out[0] = h[0] / h[1];
+  out[1] = std::sqrt(h[2] / h[3]);
+  out[2] = h[4] / h[5];
+  return DDPMA_OK;
+}
+
 extern "C" ddpma_status ddpma_rkc_step(ddpma_plan* p, int sub_id, const double* y,
                                        const double* rho, double rho_max, double h, int s_stages,
                                        double* d_out, double* fnew_out, int* flagged,

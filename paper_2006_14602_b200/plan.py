@@ -287,6 +287,23 @@ class Plan:
                                          C.byref(out)))
         return out.value
 
+    def quality(self, sub_id, psi, normalizer, sample_on_mesh):
+        psi = np.ascontiguousarray(psi, dtype=np.float64)
+        e = np.empty_like(psi)
+        rep = (C.c_double * 5)()
+        self.check(self.L.ddpma_quality(self.h, int(sub_id), _lib.dptr(psi), float(normalizer),
+                                        int(bool(sample_on_mesh)), _lib.dptr(e),
+                                        C.cast(rep, C.POINTER(C.c_double))))
+        return e, list(rep)
+
+    def relative_errors(self, sub_id, dd, sd):
+        dd = np.ascontiguousarray(dd, dtype=np.float64)
+        sd = np.ascontiguousarray(sd, dtype=np.float64)
+        out = (C.c_double * 3)()
+        self.check(self.L.ddpma_relative_errors(self.h, int(sub_id), _lib.dptr(dd), _lib.dptr(sd),
+                                                C.cast(out, C.POINTER(C.c_double))))
+        return list(out)
+
     def rkc_step(self, sub_id, y, rho, rho_max, h, s):
         y = np.ascontiguousarray(y, dtype=np.float64)
         rho = np.ascontiguousarray(np.broadcast_to(rho, y.shape), dtype=np.float64)
