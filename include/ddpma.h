@@ -46,7 +46,11 @@ enum { DDPMA_FACE_PHYSICAL = 0, DDPMA_FACE_INTERFACE = 1 };       /* grid.py:20-
 enum { DDPMA_ALTERNATING = 0, DDPMA_PARALLEL = 1 };                /* schwarz.py:41 */
 enum { DDPMA_STOP_MIN = 0, DDPMA_STOP_MAX = 1 };                   /* schwarz.py:42 */
 enum { DDPMA_SCHEME_ADAPTIVE = 0, DDPMA_SCHEME_EULER = 1 };        /* integrate.py:46 */
-enum { DDPMA_MON_UNIFORM = 0, DDPMA_MON_RING = 1, DDPMA_MON_MIXTURE = 2 };
+enum { DDPMA_MON_UNIFORM = 0, DDPMA_MON_RING = 1, DDPMA_MON_MIXTURE = 2,
+       /* arc-length monitors of the analytic test functions
+        * (arc_length_monitor monitor.py:88-97, registry :223-345): u-backed */
+       DDPMA_MON_BURGERS2D = 3, DDPMA_MON_SPIRAL2D = 4, DDPMA_MON_SPHERE3D = 5,
+       DDPMA_MON_NINE_SPHERES3D = 6, DDPMA_MON_QUASI1D_LINEAR = 7 };
 
 /* CompGrid (grid.py:24-55). extents[k] = {a_k, b_k}; counts[k] = N_k.
  * explicit_geom = 1 describes one BoxGeometry (grid.py:261-307) instead of a
@@ -80,6 +84,15 @@ typedef struct {
  *   RING    : raw = 1 + amp*exp(-sharp*|sum_k (x_k-center_k)^2 - r2|)
  *             (BASELINE ring in 2D, spherical shell in 3D)
  *   MIXTURE : raw = 1 + sum_b a_b*exp(-|x-c_b|^2 / (2 s_b^2))
+ *   BURGERS2D .. QUASI1D_LINEAR : arc-length monitors sqrt(1 + |grad u|^2)
+ *             of the named test function (monitor.py:88-97,223-327; `eps`
+ *             is burgers2d's parameter).  They carry u (MonitorField.u_fn),
+ *             so the solver's nodal density is the mesh pull-back of
+ *             mesh_density (monitor.py:151-180,183-216): u sampled on the
+ *             clamped mesh, logical np.gradient of u and of the coordinates,
+ *             |grad_x u|^2 through the adjugate of the map Jacobian.
+ *             The analytic raw (eval_clamped, normalize) is the arc length
+ *             of the analytic gradient.
  * Points are clamped into `domain` first (MonitorField.clamp, :70-74). */
 typedef struct {
   int kind;
@@ -92,7 +105,20 @@ typedef struct {
   const double* c;   /* host, nbumps*dim, row-major */
   const double* s;   /* host, nbumps */
   const double* a;   /* host, nbumps */
+  double eps;        /* burgers2d eps (> 0) */
+  int u_backed;      /* arc-length kinds: 1 = MonitorField.u_fn is set (the
+                        solver's density is the pull-back of u); 0 = the
+                        analytic raw at the clamped mesh points (e.g. after
+                        normalize(), which drops u_fn, monitor.py:147-148) */
 } ddpma_monitor;
+
+/* normalize's probe quadrature (_trapezoid_mass, monitor.py:112-120) on the
+ * device: raw (unclamped) at the nodes a_k + i*((b_k-a_k)/(n_k-1)) of the
+ * monitor's domain, composite trapezoid integral (quadrature.py:24-26) and
+ * max.  bad = 1 when any value is non-finite or <= 0 (InvalidMonitorError). */
+ddpma_status ddpma_monitor_mass(const ddpma_monitor* monitor, const int* counts,
+                                int device_ordinal, double* integral, double* peak,
+                                int* bad);
 
 /* SolverConfig (schwarz.py:35-67).  workers is meaningless on the device
  * (schedule independence is by construction) and is not carried. */

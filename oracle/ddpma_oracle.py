@@ -607,6 +607,132 @@ def seeded_mixture(nbumps, dim, seed=0):
                    tuple(float(x) for x in s), tuple(float(x) for x in a))
 
 
+# Arc-length monitors of the analytic test functions (ddmesh/monitor.py:
+# 88-97 arc_length_monitor, 223-345 the registry).  ``__call__`` is the
+# analytic raw sqrt(1 + |grad u|^2); ``u`` marks the monitor as u-backed, so
+# the solver's nodal density is the mesh pull-back (mesh_density below).
+
+_NINE = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.5], [0.5, -0.5, 0.5],
+                  [-0.5, 0.5, 0.5], [-0.5, -0.5, 0.5], [0.5, 0.5, -0.5],
+                  [0.5, -0.5, -0.5], [-0.5, 0.5, -0.5], [-0.5, -0.5, -0.5]])
+
+
+@dataclass(frozen=True)
+class ArcLength:
+    """name in {burgers2d, spiral2d, sphere3d, nine_spheres3d, quasi1d_linear}."""
+    name: str
+    eps: float = 0.01
+
+    @property
+    def domain(self):
+        if self.name == "sphere3d":
+            return ((-1.0, 1.0),) * 3
+        if self.name == "nine_spheres3d":
+            return ((-2.0, 2.0),) * 3
+        return ((0.0, 1.0), (0.0, 1.0))
+
+    def u(self, p):
+        n = self.name
+        if n == "burgers2d":                                  # monitor.py:240-243
+            a = (p[..., 0] + p[..., 1] - 1.0) / (2.0 * self.eps)
+            return 0.5 * (1.0 - np.tanh(0.5 * a))
+        if n == "spiral2d":                                   # :255-264
+            dx, dy = p[..., 0] - 0.7, p[..., 1] - 0.5
+            r2 = dx * dx + dy * dy
+            g = np.arctan2(dy, dx) - 20.0 * r2
+            return 1.0 + 9.0 / (1.0 + 100.0 * r2 * np.cos(g) ** 2)
+        if n == "sphere3d":                                   # :282-284
+            return np.tanh(100.0 * (np.sum(p * p, axis=-1) - 0.125))
+        if n == "nine_spheres3d":                             # :308-313
+            out = np.zeros(p.shape[:-1])
+            for c in _NINE:
+                d = p - c
+                out += np.tanh(50.0 * (np.sum(d * d, axis=-1) - 0.1875))
+            return out
+        x = p[..., 0]                                         # :329-333
+        w = x + 1.0
+        s = np.sqrt(np.maximum(w * w - 1.0, 0.0))
+        return 0.5 * (w * s - np.arccosh(np.maximum(w, 1.0)))
+
+    def gradient(self, p):
+        n = self.name
+        if n == "burgers2d":                                  # :245-249
+            a = (p[..., 0] + p[..., 1] - 1.0) / (2.0 * self.eps)
+            uu = 0.5 * (1.0 - np.tanh(0.5 * a))
+            d = -uu * (1.0 - uu) / (2.0 * self.eps)
+            return np.stack([d, d], axis=-1)
+        if n == "spiral2d":                                   # :266-276
+            dx, dy = p[..., 0] - 0.7, p[..., 1] - 0.5
+            r2 = dx * dx + dy * dy
+            g = np.arctan2(dy, dx) - 20.0 * r2
+            c2 = np.cos(g) ** 2
+            s2g = np.sin(2.0 * g)
+            den = 1.0 + 100.0 * r2 * c2
+            ddx = 100.0 * (2.0 * dx * c2 + dy * s2g + 40.0 * dx * r2 * s2g)
+            ddy = 100.0 * (2.0 * dy * c2 - dx * s2g + 40.0 * dy * r2 * s2g)
+            scale = -9.0 / (den * den)
+            return np.stack([np.where(r2 > 0.0, scale * ddx, 0.0),
+                             np.where(r2 > 0.0, scale * ddy, 0.0)], axis=-1)
+        if n == "sphere3d":                                   # :286-289
+            t = np.tanh(100.0 * (np.sum(p * p, axis=-1) - 0.125))
+            return (200.0 * (1.0 - t * t))[..., None] * p
+        if n == "nine_spheres3d":                             # :315-321
+            out = np.zeros_like(p)
+            for c in _NINE:
+                d = p - c
+                t = np.tanh(50.0 * (np.sum(d * d, axis=-1) - 0.1875))
+                out += (100.0 * (1.0 - t * t))[..., None] * d
+            return out
+        x = p[..., 0]                                         # :335-338
+        gx = np.sqrt(np.maximum(x * x + 2.0 * x, 0.0))
+        return np.stack([gx, np.zeros_like(gx)], axis=-1)
+
+    def __call__(self, p):                                    # monitor.py:93-95
+        g = self.gradient(p)
+        return np.sqrt(1.0 + np.sum(g * g, axis=-1))
+
+
+def _pullback_gradient_sq(gxi, jac):
+    """ddmesh/monitor.py:183-216."""
+    dim = len(gxi)
+    if dim == 2:
+        a, b = jac[0][0], jac[0][1]
+        c, d = jac[1][0], jac[1][1]
+        det = a * d - b * c
+        comps = [d * gxi[0] - c * gxi[1], -b * gxi[0] + a * gxi[1]]
+    else:
+        m = jac
+        det = (m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1])
+               - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0])
+               + m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]))
+        comps = []
+        for i in range(3):
+            i1, i2 = [r for r in range(3) if r != i]
+            acc = 0
+            for j in range(3):
+                j1, j2 = [q for q in range(3) if q != j]
+                minor = m[i1][j1] * m[i2][j2] - m[i1][j2] * m[i2][j1]
+                acc = acc + (minor if (i + j) % 2 == 0 else -minor) * gxi[j]
+            comps.append(acc)
+    g2 = sum(c * c for c in comps)
+    safe = np.abs(det) > 1e-12
+    return np.where(safe, g2 / np.where(safe, det * det, 1.0), 0.0)
+
+
+def mesh_density(mon, coords, spacing, domain):
+    """ddmesh/monitor.py:151-180 without smoothing: raw at the clamped mesh
+    nodes, or for a u-backed monitor the pull-back of u sampled there."""
+    pts = clamp(coords, domain)
+    if not hasattr(mon, "u"):
+        return mon(pts)
+    dim = coords.shape[-1]
+    u = mon.u(pts)
+    gxi = [np.gradient(u, spacing[l], axis=l, edge_order=2) for l in range(dim)]
+    jac = [[np.gradient(coords[..., k], spacing[l], axis=l, edge_order=2)
+            for l in range(dim)] for k in range(dim)]
+    return np.sqrt(1.0 + _pullback_gradient_sq(gxi, jac))
+
+
 def clamp(points, domain):
     """ddmesh/monitor.py:70-74."""
     lo = np.array([a for a, _ in domain])
@@ -708,7 +834,7 @@ def apply_traces(box, sources, dec):
 def densities(boxes, mon, domain, weights):
     """ddmesh/schwarz.py:162-192 (no smoothing / relaxation).
     Returns (rho per box, rho_max, z)."""
-    raws = [mon(clamp(b.coords, domain)) for b in boxes]
+    raws = [mesh_density(mon, b.coords, b.geom.spacing, domain) for b in boxes]
     z = 0.0
     for b, raw in zip(boxes, raws):
         z += float(np.sum(weights[b.sub.owned_g()] * raw[b.sub.owned_l()]
@@ -844,7 +970,7 @@ def solve_single(grid, mon, domain, cfg, initial=None, trace=None):
     coords, jac = mesh_of(psi, geom)
     full = tuple(slice(0, n) for n in grid.counts)
     for _ in range(cfg.max_windows):
-        raw = mon(clamp(coords, domain))
+        raw = mesh_density(mon, coords, geom.spacing, domain)
         z = float(np.sum(weights[full] * raw[full] * jac[full]))
         if not np.isfinite(z) or z <= 0.0:
             raise OracleInvalidMonitor(f"transport quadrature {z}")
@@ -882,7 +1008,8 @@ def quality_measure(psi, raw_fn, domain, normalizer, geom, sample_on_mesh=False)
     monitor.py:151-180 without smoothing)."""
     coords, jac = mesh_of(psi, geom)
     w = trap_weights(jac.shape, geom.spacing)
-    raw = raw_fn(clamp(coords, domain))
+    raw = (mesh_density(raw_fn, coords, geom.spacing, domain) if sample_on_mesh
+           else raw_fn(clamp(coords, domain)))
     if sample_on_mesh:
         rho = raw / float(np.sum(w * raw * jac))
     else:

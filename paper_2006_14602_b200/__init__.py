@@ -14,8 +14,10 @@ from .grid import (INTERFACE, PHYSICAL, BoxGeometry, CompGrid, Decomposition,
                    Subdomain, build_decomposition, build_grid, grid_geometry,
                    subdomain_geometry)
 from .integrate import IntegrationWindow, rkc_coeffs
-from .monitor import (MixtureDensity, MonitorField, RingDensity, ShellDensity,
-                      UniformDensity, density_monitor, seeded_mixture)
+from .monitor import (ArcLengthDensity, MixtureDensity, MonitorField, RingDensity,
+                      ShellDensity, TestFunction, UniformDensity, arc_length_monitor,
+                      density_monitor, normalize, seeded_mixture,
+                      test_function_registry)
 from .schwarz import (PhysicalMesh, SolverConfig, SolveResult, WindowRecord,
                       residual, solve, solve_single_domain)
 from .metrics import (ErrorReport, QualityReport, quality_measure, relative_errors,
@@ -28,6 +30,7 @@ __all__ = [
     "grid_geometry", "subdomain_geometry", "BoxGeometry", "PHYSICAL", "INTERFACE",
     "MonitorField", "density_monitor", "UniformDensity", "RingDensity",
     "ShellDensity", "MixtureDensity", "seeded_mixture",
+    "TestFunction", "ArcLengthDensity", "arc_length_monitor", "test_function_registry", "normalize",
     "IntegrationWindow", "rkc_coeffs",
     "SolverConfig", "SolveResult", "WindowRecord", "PhysicalMesh",
     "solve", "solve_single_domain", "residual",

@@ -25,6 +25,7 @@ ALTERNATING, PARALLEL = 0, 1
 STOP_MIN, STOP_MAX = 0, 1
 SCHEME_ADAPTIVE, SCHEME_EULER = 0, 1
 MON_UNIFORM, MON_RING, MON_MIXTURE = 0, 1, 2
+MON_BURGERS2D, MON_SPIRAL2D, MON_SPHERE3D, MON_NINE_SPHERES3D, MON_QUASI1D_LINEAR = 3, 4, 5, 6, 7
 NCLASS = 7
 
 
@@ -46,7 +47,8 @@ class Monitor(C.Structure):
                 ("constant", C.c_double), ("center", C.c_double * 3),
                 ("amp", C.c_double), ("sharp", C.c_double), ("r2", C.c_double),
                 ("nbumps", C.c_int), ("c", C.POINTER(C.c_double)),
-                ("s", C.POINTER(C.c_double)), ("a", C.POINTER(C.c_double))]
+                ("s", C.POINTER(C.c_double)), ("a", C.POINTER(C.c_double)),
+                ("eps", C.c_double), ("u_backed", C.c_int)]
 
 
 class SolverCfg(C.Structure):
@@ -98,6 +100,7 @@ SIGNATURES = {
     "ddpma_set_profiling": (C.c_int, [_P, C.c_int]),
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),
     "ddpma_stream": (C.c_void_p, [_P]),
+    "ddpma_monitor_mass": (C.c_int, [C.POINTER(Monitor), _I, C.c_int, _D, _D, _I]),
 }
 
 _lib = None

@@ -61,6 +61,7 @@ struct MonitorD {
   double constant;
   double center[3];
   double amp, nsharp, r2;   // nsharp = -sharp
+  double eps;               // burgers2d
   double c[MAXB * 3];
   double den[MAXB];         // (2.0*s)*s
   double a[MAXB];
@@ -145,6 +146,7 @@ struct KArgs {
   double* part;          // per-CTA partial sums
   double* part2;
   const MonitorD* mon;
+  int upull;             // 1: raw = mesh pull-back from the k_upre fields (u-backed monitor)
 };
 
 // Device-resident controller of one local subdomain: the Rkc2Integrator /
@@ -237,6 +239,20 @@ void launch_eval(const KArgs& a, int nblocks, void* stream);
 void launch_finalize(const Entry* ent, int nent, const double* part, SubRes* res,
                      int which, void* stream);
 void launch_mesh(const KArgs& a, int nblocks, int with_residual, void* stream);
+// u-backed monitors: coordinates + u(clamp(coords)) into the scratch fields
+// (d[0..2], f[1]) before a pass that reads raw with a.upull = 1.
+void launch_upre(const KArgs& a, int nblocks, void* stream);
+
+// normalize's probe lattice (monitor.py:107-120).
+struct MassArgs {
+  int dim;
+  int n[3];
+  double a[3], step[3];
+  double w_in[3], w_end[3];
+  long long nodes;
+};
+void launch_mass(const MonitorD* mon, const MassArgs& m, int nblocks, double* part, double* out,
+                 void* stream);
 void launch_prologue(const KArgs& a, int nblocks, double z, void* stream);
 void launch_res_init(SubRes* res, int n, void* stream);
 void launch_faces(const FaceJob* jobs, int njobs, int nnodes, void* stream);

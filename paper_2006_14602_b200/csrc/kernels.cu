@@ -162,6 +162,52 @@ __global__ void __launch_bounds__(256) k_finalize(const Entry* ent, const double
   }
 }
 
+// ------------------------------------------------ u-backed mesh density --
+// Scratch fields of the pull-back (free between windows: the RKC ring and
+// f_new are rebuilt by every window, integrate.py:184).
+__device__ __forceinline__ void upull_fields(const Fields& F, double** S) {
+  S[0] = F.d[0];
+  S[1] = F.d[1];
+  S[2] = F.d[2];
+  S[3] = F.f[1];
+}
+
+// Pre-pass of mesh_density's u branch (monitor.py:170-172): the mesh
+// coordinates (gradient_fd, pma.py:67-84) and u at the clamped coordinates.
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT) k_upre(const KArgs a) {
+  const int b = blockIdx.x;
+  const Entry e = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[e.sub];
+  int i0, i1, i2;
+  if (!tile_node<DIM>(g, b - e.tile_begin, i0, i1, i2)) return;
+  const long long k = lin<DIM>(g, i0, i1, i2);
+  const YAcc<DIM, YM_PLAIN> Y{&g, a.F.y[e.yi], nullptr, 0.0};
+  double* S[4];
+  upull_fields(a.F, S);
+  const MonitorD& M = *a.mon;
+  double x[3], p[3];
+#pragma unroll
+  for (int q = 0; q < DIM; ++q) {
+    x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
+    S[q][k] = x[q];
+    p[q] = clampv(x[q], M.lo[q], M.hi[q]);
+  }
+  S[DIM][k] = tf_u<DIM>(M, p);
+}
+
+// Nodal raw density: the analytic monitor at x, or the pull-back.
+template <int DIM, bool P2>
+__device__ __forceinline__ double node_raw(const KArgs& a, const SubGeo& g, int i0, int i1,
+                                           int i2, const double* x) {
+  if (a.upull) {
+    double* S[4];
+    upull_fields(a.F, S);
+    return pull_raw<DIM, P2>(a.P, g, S, i0, i1, i2);
+  }
+  return mon_raw<DIM>(*a.mon, x);
+}
+
 // ----------------------------------------------------------- mesh kernel --
 // physical_mesh (pma.py:222-225) + mesh_density (monitor.py:151-180) + the
 // owned-node transport partial w*raw*J (schwarz.py:182-186) + the window
@@ -186,7 +232,7 @@ __global__ void __launch_bounds__(NT) k_mesh(const KArgs a, int with_res) {
 #pragma unroll
     for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
     const double det = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
-    const double raw = mon_raw<DIM>(*a.mon, x);
+    const double raw = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
     a.F.raw[k] = raw;
     const int idx[3] = {i0, i1, i2};
     bool owned = true;
@@ -329,7 +375,7 @@ __global__ void __launch_bounds__(NT) k_box_mesh(const KArgs a, double* coords, 
     for (int q = 0; q < DIM; ++q) coords[dk * DIM + q] = x[q];
   }
   if (jac) jac[dk] = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
-  if (raw) raw[dk] = mon_raw<DIM>(*a.mon, x);
+  if (raw) raw[dk] = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
 }
 
 // Box <-> dense copies (operator-level API, sub_psi).
@@ -468,6 +514,18 @@ void launch_mesh(const KArgs& a, int nb, int with_res, void* stream) {
   }
 }
 
+void launch_upre(const KArgs& a, int nb, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 blk(TX, TY);
+  if (a.P.dim == 2) {
+    if (a.P.pow2) k_upre<2, true><<<nb, blk, 0, st>>>(a);
+    else k_upre<2, false><<<nb, blk, 0, st>>>(a);
+  } else {
+    if (a.P.pow2) k_upre<3, true><<<nb, blk, 0, st>>>(a);
+    else k_upre<3, false><<<nb, blk, 0, st>>>(a);
+  }
+}
+
 void launch_prologue(const KArgs& a, int nb, double z, void* stream) {
   if (nb <= 0) return;
   const dim3 blk(TX, TY);
@@ -583,7 +641,7 @@ __global__ void __launch_bounds__(NT) k_quality(const KArgs a, int mode, double 
 #pragma unroll
     for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
     const double jac = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
-    const double raw = mon_raw<DIM>(*a.mon, x);
+    const double raw = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
     const double w = box_weight<DIM>(a.P, g, i0, i1, i2);
     if (mode == 0) {
       s0 = (w * raw) * jac;
@@ -673,6 +731,60 @@ __global__ void __launch_bounds__(32) k_qfinal(const double* part, int nb, int n
     }
     out[q] = unkey(m);
   }
+}
+
+// normalize's probe quadrature (_trapezoid_mass monitor.py:112-120,
+// quadrature.integrate :24-26): values = raw(lattice) UNclamped (the
+// descriptor's clamp box is opened to +-inf by the host), w = tensor product
+// of the 1D trapezoid weights in axis order; partials {sum raw*w, #bad, -, -,
+// -, max raw key}.
+template <int DIM>
+__global__ void __launch_bounds__(NT) k_mass(const MonitorD* __restrict__ mon, const MassArgs m,
+                                             double* part) {
+  __shared__ double sh_sum[NT / 32];
+  __shared__ unsigned long long sh_u[NT / 32];
+  const long long q = (long long)blockIdx.x * NT + threadIdx.y * TX + threadIdx.x;
+  double v = 0.0, bad = 0.0;
+  unsigned long long mk = 0ull;
+  if (q < m.nodes) {
+    int idx[3];
+    long long r = q;
+#pragma unroll
+    for (int k = DIM - 1; k >= 0; --k) {
+      idx[k] = (int)(r % m.n[k]);
+      r /= m.n[k];
+    }
+    double x[3], w = 1.0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      x[k] = m.a[k] + (double)idx[k] * m.step[k];                // probe_axes (:107-109)
+      const double wk = (idx[k] == 0 || idx[k] == m.n[k] - 1) ? m.w_end[k] : m.w_in[k];
+      w = k == 0 ? wk : w * wk;                                    // np.multiply.outer order
+    }
+    const double raw = mon_raw<DIM>(*mon, x);
+    v = raw * w;
+    bad = (!isfinite(raw) || raw <= 0.0) ? 1.0 : 0.0;
+    mk = okey(raw);
+  }
+  const double vs = block_sum(v, sh_sum);
+  const double bs = block_sum(bad, sh_sum);
+  const unsigned long long mx = block_max_u64(mk, sh_u);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    double* o = part + (long long)blockIdx.x * QP_N;
+    o[0] = vs;
+    o[1] = bs;
+    o[2] = o[3] = o[4] = 0.0;
+    o[5] = __longlong_as_double((long long)mx);
+  }
+}
+
+void launch_mass(const MonitorD* mon, const MassArgs& m, int nb, double* part, double* out,
+                 void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 blk(TX, TY);
+  if (m.dim == 2) k_mass<2><<<nb, blk, 0, st>>>(mon, m, part);
+  else k_mass<3><<<nb, blk, 0, st>>>(mon, m, part);
+  k_qfinal<<<1, 32, 0, st>>>(part, nb, 5, out);
 }
 
 void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,

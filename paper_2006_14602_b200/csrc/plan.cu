@@ -124,6 +124,7 @@ struct ddpma_plan {
   Prob P{};
   MonitorD mon{};
   MonitorD* d_mon = nullptr;
+  bool u_backed = false;   // arc-length monitor carrying u (pull-back density)
   long long arena = 0;
   double* d_arena = nullptr;
   Fields F{};
@@ -285,6 +286,39 @@ KArgs base_args(ddpma_plan* p) {
   a.part2 = p->d_part2;
   a.mon = p->d_mon;
   return a;
+}
+
+// ddpma_monitor -> device descriptor.
+void fill_monitor(const ddpma_monitor* monitor, int dim, MonitorD& M) {
+  memset(&M, 0, sizeof M);
+  M.kind = monitor->kind;
+  M.dim = dim;
+  for (int k = 0; k < 3; ++k) {
+    M.lo[k] = monitor->domain[k][0];
+    M.hi[k] = monitor->domain[k][1];
+    M.center[k] = monitor->center[k];
+  }
+  M.constant = monitor->constant;
+  M.amp = monitor->amp;
+  M.nsharp = -monitor->sharp;
+  M.r2 = monitor->r2;
+  M.eps = monitor->eps;
+  M.nb = monitor->kind == DDPMA_MON_MIXTURE ? monitor->nbumps : 0;
+  for (int b = 0; b < M.nb; ++b) {
+    for (int k = 0; k < dim; ++k) M.c[b * 3 + k] = monitor->c[b * dim + k];
+    M.den[b] = 2.0 * monitor->s[b] * monitor->s[b];
+    M.a[b] = monitor->a[b];
+  }
+}
+
+// u-backed monitors (arc-length of a test function): mesh_density is the
+// mesh pull-back of u (monitor.py:170-180); run its pre-pass and let the
+// following raw-density pass read it.
+void upull_prepass(ddpma_plan* p, KArgs& a, int nb) {
+  if (p->u_backed) {
+    launch_upre(a, nb, p->st);
+    a.upull = 1;
+  }
 }
 
 Entry make_entry(ddpma_plan* p, int l) {
@@ -919,6 +953,7 @@ ddpma_status mesh_pass(ddpma_plan* p, bool with_res) {
     e1 = take_event(p);
     cudaEventRecord(e0, p->st);
   }
+  upull_prepass(p, a, nb);
   launch_mesh(a, nb, with_res ? 1 : 0, p->st);
   const long long nodes = entries_nodes(p, ents.data(), (int)ents.size());
   if (p->prof) {
@@ -1234,6 +1269,21 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     set_global_error("mixture monitor supports at most 64 bumps");
     return DDPMA_ERR_CONFIG;
   }
+  if (monitor->kind < DDPMA_MON_UNIFORM || monitor->kind > DDPMA_MON_QUASI1D_LINEAR) {
+    set_global_error("unknown monitor kind");
+    return DDPMA_ERR_CONFIG;
+  }
+  if (monitor->kind >= DDPMA_MON_BURGERS2D) {   // test-function domains (monitor.py:223-345)
+    const bool three = monitor->kind == DDPMA_MON_SPHERE3D || monitor->kind == DDPMA_MON_NINE_SPHERES3D;
+    if (grid->dim != (three ? 3 : 2)) {
+      set_global_error("grid dimension does not match monitor domain");
+      return DDPMA_ERR_CONFIG;
+    }
+    if (monitor->kind == DDPMA_MON_BURGERS2D && !(monitor->eps > 0.0)) {
+      set_global_error("burgers2d needs eps > 0");
+      return DDPMA_ERR_CONFIG;
+    }
+  }
   auto* p = new ddpma_plan();
   p->device = device;
   p->grid = *grid;
@@ -1299,25 +1349,8 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   P.atol = cfg->atol;
   P.rtol = cfg->rtol;
   // monitor
-  MonitorD& M = p->mon;
-  memset(&M, 0, sizeof M);
-  M.kind = monitor->kind;
-  M.dim = p->dim;
-  for (int k = 0; k < 3; ++k) {
-    M.lo[k] = monitor->domain[k][0];
-    M.hi[k] = monitor->domain[k][1];
-    M.center[k] = monitor->center[k];
-  }
-  M.constant = monitor->constant;
-  M.amp = monitor->amp;
-  M.nsharp = -monitor->sharp;
-  M.r2 = monitor->r2;
-  M.nb = monitor->kind == DDPMA_MON_MIXTURE ? monitor->nbumps : 0;
-  for (int b = 0; b < M.nb; ++b) {
-    for (int k = 0; k < p->dim; ++k) M.c[b * 3 + k] = monitor->c[b * p->dim + k];
-    M.den[b] = 2.0 * monitor->s[b] * monitor->s[b];
-    M.a[b] = monitor->a[b];
-  }
+  fill_monitor(monitor, p->dim, p->mon);
+  p->u_backed = monitor->kind >= DDPMA_MON_BURGERS2D && monitor->u_backed;
   // geometry + arena
   long long off = 0;
   int tiles = 0;
@@ -2031,6 +2064,7 @@ extern "C" ddpma_status ddpma_raw_density(ddpma_plan* p, int sub_id, const doubl
   KArgs a = base_args(p);
   a.ent = (Entry*)d;
   a.nent = 1;
+  upull_prepass(p, a, nb);
   launch_box_mesh(a, nb, nullptr, nullptr, p->d_scratch, p->st);
   if ((s = check_launch(p, "box_mesh raw")) != DDPMA_OK) return s;
   CK(p, cudaMemcpyAsync(raw, p->d_scratch, sizeof(double) * p->geo[l].nodes,
@@ -2070,11 +2104,75 @@ extern "C" ddpma_status ddpma_residual(ddpma_plan* p, int sub_id, const double* 
 
 // metrics kernels (kernels.cu)
 namespace ddpma {
+constexpr int QPN_MASS = 6;   // partial layout of k_mass / k_qfinal (kernels.cu QP_N)
 void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,
                     double* out, void* stream);
 void launch_relerr(const KArgs& a, int nb, const double* dd, const double* sd, double* part,
                    double* out, void* stream);
 }  // namespace ddpma
+
+extern "C" ddpma_status ddpma_monitor_mass(const ddpma_monitor* monitor, const int* counts,
+                                           int device, double* integral, double* peak,
+                                           int* bad) {
+  const int dim = monitor->dim;
+  if (dim != 2 && dim != 3) {
+    set_global_error("monitor dimension must be 2 or 3");
+    return DDPMA_ERR_CONFIG;
+  }
+  MassArgs m{};
+  m.dim = dim;
+  m.nodes = 1;
+  for (int k = 0; k < dim; ++k) {
+    if (counts[k] < 2) {
+      set_global_error("probe grid needs at least 2 nodes per axis");
+      return DDPMA_ERR_CONFIG;
+    }
+    const double a = monitor->domain[k][0], b = monitor->domain[k][1];
+    m.n[k] = counts[k];
+    m.a[k] = a;
+    m.step[k] = (b - a) / (double)(counts[k] - 1);   // probe_axes and the spacing (:109,119)
+    m.w_in[k] = m.step[k];                           // axis_weights (quadrature.py:8-13)
+    m.w_end[k] = 0.5 * m.step[k];
+    m.nodes *= counts[k];
+  }
+  MonitorD M;
+  fill_monitor(monitor, dim, M);
+  for (int k = 0; k < 3; ++k) {   // fld.raw(mesh): no clamp
+    M.lo[k] = -INFINITY;
+    M.hi[k] = INFINITY;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_global_error("cudaSetDevice failed");
+    return DDPMA_ERR_CUDA;
+  }
+  const int nb = (int)((m.nodes + NT - 1) / NT);
+  MonitorD* dm = nullptr;
+  double *part = nullptr, *out = nullptr;
+  ddpma_status s = DDPMA_OK;
+  double h[6] = {0, 0, 0, 0, 0, 0};
+  if (cudaMalloc((void**)&dm, sizeof(MonitorD)) != cudaSuccess ||
+      cudaMalloc((void**)&part, sizeof(double) * QPN_MASS * (size_t)nb) != cudaSuccess ||
+      cudaMalloc((void**)&out, sizeof(double) * 6) != cudaSuccess ||
+      cudaMemcpy(dm, &M, sizeof(MonitorD), cudaMemcpyHostToDevice) != cudaSuccess) {
+    s = DDPMA_ERR_CUDA;
+  } else {
+    launch_mass(dm, m, nb, part, out, nullptr);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpy(h, out, sizeof(double) * 6, cudaMemcpyDeviceToHost) != cudaSuccess)
+      s = DDPMA_ERR_CUDA;
+  }
+  cudaFree(dm);
+  cudaFree(part);
+  cudaFree(out);
+  if (s != DDPMA_OK) {
+    set_global_error("CUDA error in ddpma_monitor_mass");
+    return s;
+  }
+  *integral = h[0];
+  *bad = h[1] > 0.0 ? 1 : 0;
+  *peak = h[5];
+  return DDPMA_OK;
+}
 
 extern "C" ddpma_status ddpma_quality(ddpma_plan* p, int sub_id, const double* psi_host,
                                       double normalizer, int sample_on_mesh, double* e_host,
@@ -2102,6 +2200,7 @@ extern "C" ddpma_status ddpma_quality(ddpma_plan* p, int sub_id, const double* p
   double h[6] = {0, 0, 0, 0, 0, 0};
   double norm = normalizer;
   if (sample_on_mesh) {   // rho = raw / sum(w * raw * jac) (metrics.py:75-77)
+    upull_prepass(p, a, nb);  // mesh_density (metrics.py:75-76)
     launch_quality(a, nb, 0, 1.0, de, dpart, dout + 6, p->st);
     if ((s = check_launch(p, "quality z")) == DDPMA_OK &&
         cudaMemcpyAsync(h, dout + 6, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)

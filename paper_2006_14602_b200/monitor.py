@@ -128,6 +128,152 @@ def seeded_mixture(nbumps: int, dim: int, seed: int = 0) -> MixtureDensity:
                           tuple(float(x) for x in s), tuple(float(x) for x in a))
 
 
+# ------------------------------------------- arc-length test functions --
+# monitor.py:76-97 (TestFunction, arc_length_monitor) and :223-345 (the
+# analytic test functions and their registry).  The numpy bodies are the
+# reference formulas; the device restates them in stencil.cuh (tf_u/tf_grad).
+
+_UNIT_SQUARE: Extents = ((0.0, 1.0), (0.0, 1.0))
+_DOMAINS = {"burgers2d": _UNIT_SQUARE, "spiral2d": _UNIT_SQUARE,
+            "sphere3d": ((-1.0, 1.0),) * 3, "nine_spheres3d": ((-2.0, 2.0),) * 3,
+            "quasi1d_linear": _UNIT_SQUARE}
+_KIND = {"burgers2d": 3, "spiral2d": 4, "sphere3d": 5, "nine_spheres3d": 6,
+         "quasi1d_linear": 7}
+_NINE_CENTERS = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.5], [0.5, -0.5, 0.5],
+                          [-0.5, 0.5, 0.5], [-0.5, -0.5, 0.5], [0.5, 0.5, -0.5],
+                          [0.5, -0.5, -0.5], [-0.5, 0.5, -0.5], [-0.5, -0.5, -0.5]])
+
+
+def _tf_u(name: str, eps: float, p: np.ndarray) -> np.ndarray:
+    if name == "burgers2d":
+        a = (p[..., 0] + p[..., 1] - 1.0) / (2.0 * eps)
+        return 0.5 * (1.0 - np.tanh(0.5 * a))
+    if name == "spiral2d":
+        dx, dy = p[..., 0] - 0.7, p[..., 1] - 0.5
+        r2 = dx * dx + dy * dy
+        g = np.arctan2(dy, dx) - 20.0 * r2
+        return 1.0 + 9.0 / (1.0 + 100.0 * r2 * np.cos(g) ** 2)
+    if name == "sphere3d":
+        return np.tanh(100.0 * (np.sum(p * p, axis=-1) - 0.125))
+    if name == "nine_spheres3d":
+        out = np.zeros(p.shape[:-1])
+        for c in _NINE_CENTERS:
+            d = p - c
+            out += np.tanh(50.0 * (np.sum(d * d, axis=-1) - 0.1875))
+        return out
+    w = p[..., 0] + 1.0
+    s = np.sqrt(np.maximum(w * w - 1.0, 0.0))
+    return 0.5 * (w * s - np.arccosh(np.maximum(w, 1.0)))
+
+
+def _tf_grad(name: str, eps: float, p: np.ndarray) -> np.ndarray:
+    if name == "burgers2d":
+        a = (p[..., 0] + p[..., 1] - 1.0) / (2.0 * eps)
+        uu = 0.5 * (1.0 - np.tanh(0.5 * a))
+        d = -uu * (1.0 - uu) / (2.0 * eps)
+        return np.stack([d, d], axis=-1)
+    if name == "spiral2d":
+        dx, dy = p[..., 0] - 0.7, p[..., 1] - 0.5
+        r2 = dx * dx + dy * dy
+        g = np.arctan2(dy, dx) - 20.0 * r2
+        c2 = np.cos(g) ** 2
+        s2g = np.sin(2.0 * g)
+        den = 1.0 + 100.0 * r2 * c2
+        ddx = 100.0 * (2.0 * dx * c2 + dy * s2g + 40.0 * dx * r2 * s2g)
+        ddy = 100.0 * (2.0 * dy * c2 - dx * s2g + 40.0 * dy * r2 * s2g)
+        scale = -9.0 / (den * den)
+        return np.stack([np.where(r2 > 0.0, scale * ddx, 0.0),
+                         np.where(r2 > 0.0, scale * ddy, 0.0)], axis=-1)
+    if name == "sphere3d":
+        t = np.tanh(100.0 * (np.sum(p * p, axis=-1) - 0.125))
+        return (200.0 * (1.0 - t * t))[..., None] * p
+    if name == "nine_spheres3d":
+        out = np.zeros_like(p)
+        for c in _NINE_CENTERS:
+            d = p - c
+            t = np.tanh(50.0 * (np.sum(d * d, axis=-1) - 0.1875))
+            out += (100.0 * (1.0 - t * t))[..., None] * d
+        return out
+    x = p[..., 0]
+    gx = np.sqrt(np.maximum(x * x + 2.0 * x, 0.0))
+    return np.stack([gx, np.zeros_like(gx)], axis=-1)
+
+
+@dataclass(frozen=True)
+class _TfU:
+    name: str
+    eps: float
+
+    def __call__(self, p):
+        return _tf_u(self.name, self.eps, np.asarray(p, dtype=float))
+
+
+@dataclass(frozen=True)
+class _TfGrad:
+    name: str
+    eps: float
+
+    def __call__(self, p):
+        return _tf_grad(self.name, self.eps, np.asarray(p, dtype=float))
+
+
+@dataclass(frozen=True)
+class TestFunction:
+    """Closed-form physical solution u with its analytic gradient (monitor.py:76-84)."""
+    __test__ = False   # not a pytest class
+
+    name: str
+    domain: Extents
+    u: Callable[[np.ndarray], np.ndarray]
+    gradient: Callable[[np.ndarray], np.ndarray]
+    params: dict = field(default_factory=dict)
+
+
+@dataclass(frozen=True)
+class ArcLengthDensity:
+    """raw = sqrt(1 + |grad u|^2) of a registered test function
+    (arc_length_monitor's raw, monitor.py:92-95); device kinds 3..7."""
+    name: str
+    eps: float = 0.01
+
+    def __call__(self, p):
+        g = _tf_grad(self.name, self.eps, np.asarray(p, dtype=float))
+        return np.sqrt(1.0 + np.sum(g * g, axis=-1))
+
+
+def test_function_registry(name: str, **params) -> TestFunction:
+    """Named analytic test functions with gradients and domains (monitor.py:341-357)."""
+    if name not in _KIND:
+        raise ConfigurationError(
+            f"unknown test function {name!r}; known: {sorted(_KIND)}")
+    eps = 0.0
+    extra = {}
+    if name == "burgers2d":
+        eps = float(params.pop("eps", 0.01))
+        if eps <= 0.0:
+            raise ConfigurationError(f"burgers2d needs eps > 0, got {eps}")
+        if params:
+            raise ConfigurationError(f"unknown parameters {sorted(params)}")
+        extra = {"eps": eps}
+    elif params:
+        raise ConfigurationError(f"{name} takes no parameters, got {sorted(params)}")
+    return TestFunction(name, _DOMAINS[name], _TfU(name, eps), _TfGrad(name, eps), extra)
+
+
+test_function_registry.__test__ = False   # not a pytest function
+
+
+def arc_length_monitor(source: TestFunction) -> MonitorField:
+    """Unnormalised arc-length density of ``source`` (monitor.py:88-97); u-backed,
+    so the solver's nodal density is the mesh pull-back of u (mesh_density)."""
+    if not isinstance(source, TestFunction) or not isinstance(source.u, _TfU):
+        raise ConfigurationError(
+            "the device path supports arc-length monitors of the registered analytic "
+            "test functions (test_function_registry); sampled fields are not supported")
+    return MonitorField(raw=ArcLengthDensity(source.u.name, source.u.eps),
+                        domain=source.domain, u_fn=source.u)
+
+
 @dataclass
 class NativeMonitor:
     """A MonitorField lowered to the C descriptor (keeps buffers alive)."""
@@ -139,10 +285,11 @@ def lower_monitor(mon: MonitorField, dim: int) -> NativeMonitor:
     """MonitorField -> ddpma_monitor, or ConfigurationError (no CPU fallback)."""
     if not isinstance(mon, MonitorField):
         raise ConfigurationError("monitor must be a MonitorField")
-    if mon.u_fn is not None:
+    if mon.u_fn is not None and not (isinstance(mon.raw, ArcLengthDensity)
+                                     and mon.u_fn == _TfU(mon.raw.name, mon.raw.eps)):
         raise ConfigurationError(
-            "monitors backed by a physical scalar u (arc-length / sampled fields) "
-            "are not supported on the device path yet")
+            "monitors backed by a physical scalar u are supported for the registered "
+            "analytic test functions (arc_length_monitor); sampled fields are not")
     if mon.dim != dim:
         raise ConfigurationError("grid dimension does not match monitor domain")
     d = _lib.Monitor()
@@ -161,6 +308,15 @@ def lower_monitor(mon: MonitorField, dim: int) -> NativeMonitor:
         for k in range(dim):
             d.center[k] = float(raw.center[k])
         d.amp, d.sharp, d.r2 = float(raw.amp), float(raw.sharp), float(raw.r2)
+    elif isinstance(raw, ArcLengthDensity):
+        # u_fn set: the solver's density is the pull-back of u (mesh_density
+        # monitor.py:170-180); absent (normalize() drops it, :147-148): the
+        # analytic arc length at the clamped mesh points (:166-168)
+        d.kind = _KIND[raw.name]
+        d.eps = float(raw.eps)
+        d.u_backed = 1 if mon.u_fn is not None else 0
+        if len(_DOMAINS[raw.name]) != dim:
+            raise ConfigurationError("grid dimension does not match monitor domain")
     elif isinstance(raw, MixtureDensity):
         c = np.ascontiguousarray(np.array(raw.c, dtype=np.float64).reshape(-1, dim))
         s = np.ascontiguousarray(np.array(raw.s, dtype=np.float64))
@@ -179,3 +335,41 @@ def lower_monitor(mon: MonitorField, dim: int) -> NativeMonitor:
             "ShellDensity, MixtureDensity); arbitrary Python callables cannot run "
             "on the GPU and there is no CPU fallback")
     return NativeMonitor(d, keep)
+
+
+def _device_mass(mon: MonitorField, counts: tuple[int, ...]) -> tuple[float, float]:
+    """_trapezoid_mass (monitor.py:112-120) on the device."""
+    nm = lower_monitor(MonitorField(raw=mon.raw, domain=mon.domain), mon.dim)
+    cnt = (C.c_int * 3)(*(list(counts) + [1] * (3 - len(counts))))
+    z, peak, bad = C.c_double(), C.c_double(), C.c_int()
+    import torch
+    st = _lib.lib().ddpma_monitor_mass(C.byref(nm.desc), cnt, int(torch.cuda.current_device()),
+                                       C.byref(z), C.byref(peak), C.byref(bad))
+    _lib.check_global(st)
+    if bad.value:
+        from .errors import InvalidMonitorError
+        raise InvalidMonitorError("density is nonpositive or non-finite on Omega")
+    return z.value, peak.value
+
+
+def normalize(fld: MonitorField, grid, z_rtol: float = 1e-5) -> MonitorField:
+    """Normalise by converged composite-trapezoid quadrature on refined probe
+    grids (monitor.py:123-148); the probe sums run on the device.  Like the
+    reference, the result carries no ``u_fn``."""
+    from .errors import InvalidMonitorError
+    if len(grid.counts) != fld.dim:
+        raise ConfigurationError("grid dimension does not match monitor domain")
+    _lib.require_cuda()
+    cap = 4097 if fld.dim == 2 else 257
+    counts = tuple(grid.counts)
+    z, peak = _device_mass(fld, counts)
+    while max(counts) < cap:
+        counts = tuple(min(cap, 2 * n - 1) for n in counts)
+        z_new, peak = _device_mass(fld, counts)
+        done = abs(z_new - z) <= z_rtol * abs(z_new)
+        z = z_new
+        if done:
+            break
+    if not np.isfinite(z) or z <= 0.0:
+        raise InvalidMonitorError(f"quadrature of the density is {z}")
+    return MonitorField(raw=fld.raw, domain=fld.domain, normalizer=z, max_value=peak / z)
