@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v \
            -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude
 CXXFLAGS := -O2 -fPIC -std=c++17 -ffp-contract=off -Iinclude
 
-OBJ := build/decomp.o build/plan.o build/kernels.o build/persist.o
+OBJ := build/decomp.o build/plan.o build/kernels.o build/persist.o build/fileio.o
 
 all: $(OUT)
 
@@ -23,6 +23,9 @@ build:
 
 build/decomp.o: $(SRC)/decomp.cpp $(SRC)/ddpma_internal.h include/ddpma.h | build
 	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+build/fileio.o: $(SRC)/fileio.cpp include/ddpma.h | build
+	$(CXX) $(CXXFLAGS) -pthread -c $< -o $@
 
 build/plan.o: $(SRC)/plan.cu $(SRC)/ddpma_internal.h include/ddpma.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/plan.ptxas.log || (cat build/plan.ptxas.log; false)
@@ -34,7 +37,7 @@ build/persist.o: $(SRC)/persist.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/persist.ptxas.log || (cat build/persist.ptxas.log; false)
 
 $(OUT): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -Xcompiler -pthread
 
 clean:
 	rm -rf build $(OUT)

@@ -39,7 +39,8 @@ typedef enum {
    * spectral radius estimate is NaN / inf: int(np.ceil(nan)) and
    * int(np.ceil(inf)) in _stages_for (integrate.py:160). */
   DDPMA_ERR_VALUE = 6,            /* ValueError    */
-  DDPMA_ERR_OVERFLOW = 7          /* OverflowError */
+  DDPMA_ERR_OVERFLOW = 7,         /* OverflowError */
+  DDPMA_ERR_IO = 8                /* OSError (file writers)             */
 } ddpma_status;
 
 enum { DDPMA_FACE_PHYSICAL = 0, DDPMA_FACE_INTERFACE = 1 };       /* grid.py:20-21 */
@@ -134,6 +135,11 @@ typedef struct {
   double atol;
   int max_stages;
   double det_floor;
+  /* _window_densities (schwarz.py:162-192): per-axis [1,2,1]/4 smoothing
+   * passes of each box's nodal density (monitor._smooth, monitor.py:395-409)
+   * and the blend weight of the previous window's density. */
+  int monitor_smooth_passes;
+  double monitor_relax;
 } ddpma_solver_cfg;
 
 typedef struct ddpma_plan ddpma_plan;
@@ -312,6 +318,20 @@ ddpma_status ddpma_profile(const ddpma_plan* plan, double* ms, double* bytes,
 
 /* The CUDA stream all plan work runs on (cudaStream_t as void*). */
 void* ddpma_stream(const ddpma_plan* plan);
+
+/* ------------------------------------------------------ output formats ---
+ * write_mesh_vtk (fileio.py:45-68): legacy-VTK structured grid, x fastest,
+ * 17 significant digits, byte-identical to the reference writer.  coords is
+ * the C-order [..., dim] array of a SolveResult mesh (host), jac the
+ * first point scalar (named `first_scalar`: "jacobian", or the field name of
+ * write_scalar_field_vtk :71-80), e_adp optional (NULL).  Rows are formatted
+ * on all host threads. */
+ddpma_status ddpma_write_mesh_vtk(const char* path, int dim, const int* counts,
+                                  const double* coords, const double* jac,
+                                  const double* e_adp, const char* title,
+                                  const char* first_scalar);
+/* Message of the last failed file operation on this thread. */
+const char* ddpma_io_error(void);
 
 #ifdef __cplusplus
 }

@@ -719,9 +719,26 @@ def _pullback_gradient_sq(gxi, jac):
     return np.where(safe, g2 / np.where(safe, det * det, 1.0), 0.0)
 
 
-def mesh_density(mon, coords, spacing, domain):
-    """ddmesh/monitor.py:151-180 without smoothing: raw at the clamped mesh
-    nodes, or for a u-backed monitor the pull-back of u sampled there."""
+def smooth(values, passes):
+    """ddmesh/monitor.py:395-409: per-axis [1,2,1]/4 with reflected edges."""
+    out = values
+    for _ in range(passes):
+        for axis in range(out.ndim):
+            n = out.shape[axis]
+            left = np.take(out, [1] + list(range(0, n - 1)), axis=axis)
+            right = np.take(out, list(range(1, n)) + [n - 2], axis=axis)
+            out = 0.25 * left + 0.5 * out + 0.25 * right
+    return out
+
+
+def mesh_density(mon, coords, spacing, domain, smooth_passes=0):
+    """ddmesh/monitor.py:151-180: raw at the clamped mesh nodes, or for a
+    u-backed monitor the pull-back of u sampled there; then smoothing."""
+    rho = _mesh_density(mon, coords, spacing, domain)
+    return smooth(rho, smooth_passes) if smooth_passes else rho
+
+
+def _mesh_density(mon, coords, spacing, domain):
     pts = clamp(coords, domain)
     if not hasattr(mon, "u"):
         return mon(pts)
@@ -757,6 +774,8 @@ class Config:
     atol: float = 1e-6
     max_stages: int = 512
     det_floor: float = DET_FLOOR
+    monitor_smooth_passes: int = 0
+    monitor_relax: float = 0.0
 
 
 @dataclass
@@ -769,6 +788,7 @@ class Box:
     mask: np.ndarray
     stepper: object
     res: float = np.inf
+    rho_raw: object = None
 
 
 @dataclass
@@ -831,10 +851,15 @@ def apply_traces(box, sources, dec):
         box.psi[tuple(dst)] = sources[donor][tuple(src)]
 
 
-def densities(boxes, mon, domain, weights):
-    """ddmesh/schwarz.py:162-192 (no smoothing / relaxation).
-    Returns (rho per box, rho_max, z)."""
-    raws = [mesh_density(mon, b.coords, b.geom.spacing, domain) for b in boxes]
+def densities(boxes, mon, domain, weights, smooth_passes=0, relax=0.0):
+    """ddmesh/schwarz.py:162-192.  Returns (rho per box, rho_max, z)."""
+    raws = [mesh_density(mon, b.coords, b.geom.spacing, domain, smooth_passes)
+            for b in boxes]
+    if relax > 0.0:
+        raws = [raw if b.rho_raw is None else (1.0 - relax) * raw + relax * b.rho_raw
+                for b, raw in zip(boxes, raws)]
+    for b, raw in zip(boxes, raws):
+        b.rho_raw = raw
     z = 0.0
     for b, raw in zip(boxes, raws):
         z += float(np.sum(weights[b.sub.owned_g()] * raw[b.sub.owned_l()]
@@ -860,7 +885,8 @@ def advance_box(box, rho, rho_max, cfg, psi_n, counter, lock=None):
 
 def sweep(boxes, mon, domain, cfg, dec, weights, counter, pool=None, lock=None):
     """ddmesh/schwarz.py:216-268 (alternating or parallel)."""
-    rho, rmax, _ = densities(boxes, mon, domain, weights)
+    rho, rmax, _ = densities(boxes, mon, domain, weights, cfg.monitor_smooth_passes,
+                             cfg.monitor_relax)
     if cfg.transmission == "alternating":
         src = [b.psi for b in boxes]
         for b in boxes:
@@ -969,8 +995,12 @@ def solve_single(grid, mon, domain, cfg, initial=None, trace=None):
     res = np.inf
     coords, jac = mesh_of(psi, geom)
     full = tuple(slice(0, n) for n in grid.counts)
+    rho_prev = None
     for _ in range(cfg.max_windows):
-        raw = mesh_density(mon, coords, geom.spacing, domain)
+        raw = mesh_density(mon, coords, geom.spacing, domain, cfg.monitor_smooth_passes)
+        if cfg.monitor_relax > 0.0 and rho_prev is not None:
+            raw = (1.0 - cfg.monitor_relax) * raw + cfg.monitor_relax * rho_prev
+        rho_prev = raw
         z = float(np.sum(weights[full] * raw[full] * jac[full]))
         if not np.isfinite(z) or z <= 0.0:
             raise OracleInvalidMonitor(f"transport quadrature {z}")
@@ -1001,14 +1031,15 @@ def solve_single(grid, mon, domain, cfg, initial=None, trace=None):
 
 # ------------------------------------------------------------ metrics ----
 
-def quality_measure(psi, raw_fn, domain, normalizer, geom, sample_on_mesh=False):
+def quality_measure(psi, raw_fn, domain, normalizer, geom, sample_on_mesh=False,
+                    smooth_passes=0):
     """ddmesh/metrics.py:57-85 (no smoothing): -> (e_adp, e2, emax, node_mean,
     tangled).  rho = raw(clamp(x)) / normalizer (monitor.py:66-68), or with
     sample_on_mesh raw / sum(w raw J) (metrics.py:75-77, mesh_density
     monitor.py:151-180 without smoothing)."""
     coords, jac = mesh_of(psi, geom)
     w = trap_weights(jac.shape, geom.spacing)
-    raw = (mesh_density(raw_fn, coords, geom.spacing, domain) if sample_on_mesh
+    raw = (mesh_density(raw_fn, coords, geom.spacing, domain, smooth_passes) if sample_on_mesh
            else raw_fn(clamp(coords, domain)))
     if sample_on_mesh:
         rho = raw / float(np.sum(w * raw * jac))

@@ -20,6 +20,8 @@ from .monitor import (ArcLengthDensity, MixtureDensity, MonitorField, RingDensit
                       test_function_registry)
 from .schwarz import (PhysicalMesh, SolverConfig, SolveResult, WindowRecord,
                       residual, solve, solve_single_domain)
+from .fileio import (read_mesh_vtk, read_scalar_field_vtk, write_field_csv, write_mesh_vtk,
+                     write_scalar_field_vtk)
 from .metrics import (ErrorReport, QualityReport, quality_measure, relative_errors,
                       restrict_to_grid)
 
@@ -36,5 +38,7 @@ __all__ = [
     "solve", "solve_single_domain", "residual",
     "DdmeshError", "ConfigurationError", "DomainError", "InvalidMonitorError",
     "MeshFileError", "StiffnessError",
+    "write_mesh_vtk", "write_scalar_field_vtk", "write_field_csv", "read_mesh_vtk",
+    "read_scalar_field_vtk",
     "QualityReport", "ErrorReport", "quality_measure", "relative_errors", "restrict_to_grid",
 ]

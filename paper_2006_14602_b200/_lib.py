@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DDPMA_LIB") or os.path.join(_HERE, "libddpma.so")
 
 OK, ERR_CONFIG, ERR_INVALID_MONITOR, ERR_STIFFNESS, ERR_CUDA, ERR_STATE, ERR_VALUE, \
-    ERR_OVERFLOW = range(8)
+    ERR_OVERFLOW, ERR_IO = range(9)
 FACE_PHYSICAL, FACE_INTERFACE = 0, 1
 ALTERNATING, PARALLEL = 0, 1
 STOP_MIN, STOP_MAX = 0, 1
@@ -55,7 +55,8 @@ class SolverCfg(C.Structure):
     _fields_ = [("dtau", C.c_double), ("tol", C.c_double), ("transmission", C.c_int),
                 ("stop_rule", C.c_int), ("max_windows", C.c_int), ("scheme", C.c_int),
                 ("substeps", C.c_int), ("rtol", C.c_double), ("atol", C.c_double),
-                ("max_stages", C.c_int), ("det_floor", C.c_double)]
+                ("max_stages", C.c_int), ("det_floor", C.c_double),
+                ("monitor_smooth_passes", C.c_int), ("monitor_relax", C.c_double)]
 
 
 _P = C.c_void_p
@@ -101,6 +102,9 @@ SIGNATURES = {
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),
     "ddpma_stream": (C.c_void_p, [_P]),
     "ddpma_monitor_mass": (C.c_int, [C.POINTER(Monitor), _I, C.c_int, _D, _D, _I]),
+    "ddpma_write_mesh_vtk": (C.c_int, [C.c_char_p, C.c_int, _I, _D, _D, _D, C.c_char_p,
+                                       C.c_char_p]),
+    "ddpma_io_error": (C.c_char_p, []),
 }
 
 _lib = None
@@ -138,6 +142,8 @@ def raise_status(st: int, msg: str):
         raise StiffnessError(msg)
     if st == ERR_VALUE:
         raise ValueError(msg)
+    if st == ERR_IO:
+        raise OSError(msg)
     if st == ERR_OVERFLOW:
         raise OverflowError(msg)
     raise DdmeshError(msg)

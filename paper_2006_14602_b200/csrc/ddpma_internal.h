@@ -239,6 +239,12 @@ void launch_eval(const KArgs& a, int nblocks, void* stream);
 void launch_finalize(const Entry* ent, int nent, const double* part, SubRes* res,
                      int which, void* stream);
 void launch_mesh(const KArgs& a, int nblocks, int with_residual, void* stream);
+// k_mesh with the density from smoothing buffer `src` (0: evaluate) and the
+// relaxation blend (schwarz.py:162-192); buffers: 1 = mr, 2 = y[1-yi].
+void launch_mesh_ex(const KArgs& a, int nblocks, int with_residual, int src, double relax,
+                    int blend, void* stream);
+void launch_rawfill(const KArgs& a, int nblocks, int dst, void* stream);
+void launch_smooth(const KArgs& a, int nblocks, int axis, int src, int dst, void* stream);
 // u-backed monitors: coordinates + u(clamp(coords)) into the scratch fields
 // (d[0..2], f[1]) before a pass that reads raw with a.upull = 1.
 void launch_upre(const KArgs& a, int nblocks, void* stream);

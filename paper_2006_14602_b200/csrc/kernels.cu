@@ -212,8 +212,53 @@ __device__ __forceinline__ double node_raw(const KArgs& a, const SubGeo& g, int 
 // physical_mesh (pma.py:222-225) + mesh_density (monitor.py:151-180) + the
 // owned-node transport partial w*raw*J (schwarz.py:182-186) + the window
 // residual (psi - psi_level_n)^2 * w_box (schwarz.py:111-115) + J min/max.
+// Smoothing / relaxation buffers (free between windows: mr is rebuilt by the
+// prologue, y[1-yi] is the integrator's candidate slot).
+__device__ __forceinline__ double* dens_buf(const KArgs& a, const Entry& e, int sel) {
+  return sel == 1 ? a.F.mr : a.F.y[1 - e.yi];
+}
+
+// Nodal raw density into a smoothing buffer (mesh_density before _smooth).
 template <int DIM, bool P2>
-__global__ void __launch_bounds__(NT) k_mesh(const KArgs a, int with_res) {
+__global__ void __launch_bounds__(NT) k_rawfill(const KArgs a, int dst) {
+  const int b = blockIdx.x;
+  const Entry e = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[e.sub];
+  int i0, i1, i2;
+  if (!tile_node<DIM>(g, b - e.tile_begin, i0, i1, i2)) return;
+  const YAcc<DIM, YM_PLAIN> Y{&g, a.F.y[e.yi], nullptr, 0.0};
+  double x[3];
+#pragma unroll
+  for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
+  dens_buf(a, e, dst)[lin<DIM>(g, i0, i1, i2)] = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
+}
+
+// One axis of monitor._smooth (monitor.py:395-409): reflected edges
+// (out[1] before index 0, out[-2] after n-1), 0.25*left + 0.5*mid + 0.25*right.
+template <int DIM>
+__global__ void __launch_bounds__(NT) k_smooth(const KArgs a, int axis, int src, int dst) {
+  const int b = blockIdx.x;
+  const Entry e = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[e.sub];
+  int i0, i1, i2;
+  if (!tile_node<DIM>(g, b - e.tile_begin, i0, i1, i2)) return;
+  const double* __restrict__ s = dens_buf(a, e, src);
+  int idx[3] = {i0, i1, i2};
+  const int n = g.n[axis], i = idx[axis];
+  const int il = i == 0 ? 1 : i - 1, ir = i == n - 1 ? n - 2 : i + 1;
+  idx[axis] = il;
+  const double left = s[lin<DIM>(g, idx[0], idx[1], idx[2])];
+  idx[axis] = ir;
+  const double right = s[lin<DIM>(g, idx[0], idx[1], idx[2])];
+  const long long k = lin<DIM>(g, i0, i1, i2);
+  dens_buf(a, e, dst)[k] = (0.25 * left + 0.5 * s[k]) + 0.25 * right;
+}
+
+// src: 0 = evaluate the density here, else the smoothing buffer holding it;
+// blend: (1-relax)*raw + relax*previous raw (schwarz.py:176-179).
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT) k_mesh(const KArgs a, int with_res, int src, double relax,
+                                             int blend) {
   __shared__ double sh_sum[NT / 32];
   __shared__ unsigned long long sh_u[NT / 32];
   const int b = blockIdx.x;
@@ -232,7 +277,8 @@ __global__ void __launch_bounds__(NT) k_mesh(const KArgs a, int with_res) {
 #pragma unroll
     for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
     const double det = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
-    const double raw = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
+    double raw = src ? dens_buf(a, e, src)[k] : node_raw<DIM, P2>(a, g, i0, i1, i2, x);
+    if (blend) raw = (1.0 - relax) * raw + relax * a.F.raw[k];
     a.F.raw[k] = raw;
     const int idx[3] = {i0, i1, i2};
     bool owned = true;
@@ -502,16 +548,42 @@ void launch_finalize(const Entry* ent, int nent, const double* part, SubRes* res
 }
 
 void launch_mesh(const KArgs& a, int nb, int with_res, void* stream) {
+  launch_mesh_ex(a, nb, with_res, 0, 0.0, 0, stream);
+}
+
+void launch_mesh_ex(const KArgs& a, int nb, int with_res, int src, double relax, int blend,
+                    void* stream) {
   if (nb <= 0) return;
   const dim3 blk(TX, TY);
   cudaStream_t st = (cudaStream_t)stream;
   if (a.P.dim == 2) {
-    if (a.P.pow2) k_mesh<2, true><<<nb, blk, 0, st>>>(a, with_res);
-    else k_mesh<2, false><<<nb, blk, 0, st>>>(a, with_res);
+    if (a.P.pow2) k_mesh<2, true><<<nb, blk, 0, st>>>(a, with_res, src, relax, blend);
+    else k_mesh<2, false><<<nb, blk, 0, st>>>(a, with_res, src, relax, blend);
   } else {
-    if (a.P.pow2) k_mesh<3, true><<<nb, blk, 0, st>>>(a, with_res);
-    else k_mesh<3, false><<<nb, blk, 0, st>>>(a, with_res);
+    if (a.P.pow2) k_mesh<3, true><<<nb, blk, 0, st>>>(a, with_res, src, relax, blend);
+    else k_mesh<3, false><<<nb, blk, 0, st>>>(a, with_res, src, relax, blend);
   }
+}
+
+void launch_rawfill(const KArgs& a, int nb, int dst, void* stream) {
+  if (nb <= 0) return;
+  const dim3 blk(TX, TY);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.P.dim == 2) {
+    if (a.P.pow2) k_rawfill<2, true><<<nb, blk, 0, st>>>(a, dst);
+    else k_rawfill<2, false><<<nb, blk, 0, st>>>(a, dst);
+  } else {
+    if (a.P.pow2) k_rawfill<3, true><<<nb, blk, 0, st>>>(a, dst);
+    else k_rawfill<3, false><<<nb, blk, 0, st>>>(a, dst);
+  }
+}
+
+void launch_smooth(const KArgs& a, int nb, int axis, int src, int dst, void* stream) {
+  if (nb <= 0) return;
+  const dim3 blk(TX, TY);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.P.dim == 2) k_smooth<2><<<nb, blk, 0, st>>>(a, axis, src, dst);
+  else k_smooth<3><<<nb, blk, 0, st>>>(a, axis, src, dst);
 }
 
 void launch_upre(const KArgs& a, int nb, void* stream) {
@@ -625,7 +697,7 @@ constexpr int QP_N = 6;
 //         {sum (w*e)*e, sum w, max|e| key, sum e, nonpositive jac count, NaN seen}
 template <int DIM, bool P2>
 __global__ void __launch_bounds__(NT) k_quality(const KArgs a, int mode, double norm,
-                                                double* e_out, double* part) {
+                                                double* e_out, double* part, int src) {
   __shared__ double sh_sum[NT / 32];
   __shared__ unsigned long long sh_u[NT / 32];
   const int b = blockIdx.x;
@@ -641,7 +713,8 @@ __global__ void __launch_bounds__(NT) k_quality(const KArgs a, int mode, double 
 #pragma unroll
     for (int q = 0; q < DIM; ++q) x[q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
     const double jac = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
-    const double raw = node_raw<DIM, P2>(a, g, i0, i1, i2, x);
+    const double raw = src ? dens_buf(a, en, src)[lin<DIM>(g, i0, i1, i2)]
+                           : node_raw<DIM, P2>(a, g, i0, i1, i2, x);
     const double w = box_weight<DIM>(a.P, g, i0, i1, i2);
     if (mode == 0) {
       s0 = (w * raw) * jac;
@@ -788,16 +861,16 @@ void launch_mass(const MonitorD* mon, const MassArgs& m, int nb, double* part, d
 }
 
 void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,
-                    double* out, void* stream) {
+                    double* out, void* stream, int src) {
   if (nb <= 0) return;
   const dim3 blk(TX, TY);
   cudaStream_t st = (cudaStream_t)stream;
   if (a.P.dim == 2) {
-    if (a.P.pow2) k_quality<2, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
-    else k_quality<2, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+    if (a.P.pow2) k_quality<2, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part, src);
+    else k_quality<2, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part, src);
   } else {
-    if (a.P.pow2) k_quality<3, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
-    else k_quality<3, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part);
+    if (a.P.pow2) k_quality<3, true><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part, src);
+    else k_quality<3, false><<<nb, blk, 0, st>>>(a, mode, norm, e_out, part, src);
   }
   k_qfinal<<<1, 32, 0, st>>>(part, nb, 5, out);
 }

@@ -144,6 +144,7 @@ struct ddpma_plan {
   bool state_set = false;
   bool density_ready = false;
   bool have_old = false;
+  bool raw_valid = false;   // F.raw holds the previous window's density (monitor_relax)
   double z = 0.0, rho_max = 0.0;
   std::vector<double> zpart, rawmax, resid, jmin, jmax;
   // errors
@@ -953,8 +954,21 @@ ddpma_status mesh_pass(ddpma_plan* p, bool with_res) {
     e1 = take_event(p);
     cudaEventRecord(e0, p->st);
   }
+  // _window_densities (schwarz.py:162-192): density, smoothing, relaxation
+  int src = 0;
   upull_prepass(p, a, nb);
-  launch_mesh(a, nb, with_res ? 1 : 0, p->st);
+  if (p->cfg.monitor_smooth_passes > 0) {
+    launch_rawfill(a, nb, 1, p->st);
+    src = 1;
+    for (int pass = 0; pass < p->cfg.monitor_smooth_passes; ++pass)
+      for (int ax = 0; ax < p->dim; ++ax) {
+        launch_smooth(a, nb, ax, src, 3 - src, p->st);
+        src = 3 - src;
+      }
+  }
+  const int blend = p->cfg.monitor_relax > 0.0 && p->raw_valid ? 1 : 0;
+  launch_mesh_ex(a, nb, with_res ? 1 : 0, src, p->cfg.monitor_relax, blend, p->st);
+  p->raw_valid = true;
   const long long nodes = entries_nodes(p, ents.data(), (int)ents.size());
   if (p->prof) {
     cudaEventRecord(e1, p->st);
@@ -1600,6 +1614,7 @@ extern "C" ddpma_status ddpma_set_state(ddpma_plan* p, const double* psi_global_
   p->state_set = true;
   p->density_ready = false;
   p->have_old = false;
+  p->raw_valid = false;
   p->fail = Failure{};
   return sync(p);
 }
@@ -2106,7 +2121,7 @@ extern "C" ddpma_status ddpma_residual(ddpma_plan* p, int sub_id, const double* 
 namespace ddpma {
 constexpr int QPN_MASS = 6;   // partial layout of k_mass / k_qfinal (kernels.cu QP_N)
 void launch_quality(const KArgs& a, int nb, int mode, double norm, double* e_out, double* part,
-                    double* out, void* stream);
+                    double* out, void* stream, int src);
 void launch_relerr(const KArgs& a, int nb, const double* dd, const double* sd, double* part,
                    double* out, void* stream);
 }  // namespace ddpma
@@ -2199,9 +2214,19 @@ extern "C" ddpma_status ddpma_quality(ddpma_plan* p, int sub_id, const double* p
   a.nent = 1;
   double h[6] = {0, 0, 0, 0, 0, 0};
   double norm = normalizer;
+  int qsrc = 0;
   if (sample_on_mesh) {   // rho = raw / sum(w * raw * jac) (metrics.py:75-77)
     upull_prepass(p, a, nb);  // mesh_density (metrics.py:75-76)
-    launch_quality(a, nb, 0, 1.0, de, dpart, dout + 6, p->st);
+    if (p->cfg.monitor_smooth_passes > 0) {   // its smooth_passes (monitor.py:178-179)
+      launch_rawfill(a, nb, 1, p->st);
+      qsrc = 1;
+      for (int pass = 0; pass < p->cfg.monitor_smooth_passes; ++pass)
+        for (int ax = 0; ax < p->dim; ++ax) {
+          launch_smooth(a, nb, ax, qsrc, 3 - qsrc, p->st);
+          qsrc = 3 - qsrc;
+        }
+    }
+    launch_quality(a, nb, 0, 1.0, de, dpart, dout + 6, p->st, qsrc);
     if ((s = check_launch(p, "quality z")) == DDPMA_OK &&
         cudaMemcpyAsync(h, dout + 6, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)
       s = DDPMA_ERR_CUDA;
@@ -2209,7 +2234,7 @@ extern "C" ddpma_status ddpma_quality(ddpma_plan* p, int sub_id, const double* p
     norm = h[0];
   }
   if (s == DDPMA_OK) {
-    launch_quality(a, nb, 1, norm, de, dpart, dout, p->st);
+    launch_quality(a, nb, 1, norm, de, dpart, dout, p->st, qsrc);
     s = check_launch(p, "quality");
   }
   if (s == DDPMA_OK && cudaMemcpyAsync(h, dout, sizeof(double) * 6, cudaMemcpyDeviceToHost, p->st) != cudaSuccess)

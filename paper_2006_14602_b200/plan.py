@@ -30,6 +30,8 @@ def _cfg_to_c(config) -> _lib.SolverCfg:
     c.atol = float(config.atol)
     c.max_stages = int(config.max_stages)
     c.det_floor = float(config.det_floor)
+    c.monitor_smooth_passes = max(0, int(config.monitor_smooth_passes))
+    c.monitor_relax = float(config.monitor_relax)
     return c
 
 

@@ -105,10 +105,6 @@ class SolveResult:
 
 def _validate(config: SolverConfig):
     config.window()   # IntegrationWindow validation (integrate.py:52-60)
-    if config.monitor_smooth_passes or config.monitor_relax:
-        raise ConfigurationError(
-            "monitor_smooth_passes / monitor_relax are not supported on the device "
-            "path yet (SURVEY §8(f) row 3)")
 
 
 def _history(hist_res, hist_stats):

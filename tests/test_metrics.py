@@ -81,9 +81,6 @@ def test_device_metrics_errors_and_restrict():
         P.restrict_to_grid(np.zeros((65, 65)), (40, 40))
     fine = np.arange(129 * 129, dtype=float).reshape(129, 129)
     assert np.array_equal(P.restrict_to_grid(fine, (65, 65)), fine[::2, ::2])
-    mon = P.density_monitor(P.RingDensity(), grid.extents)
-    with pytest.raises(P.ConfigurationError):
-        P.quality_measure(np.zeros((65, 65)), mon, grid, smooth_passes=1)
     # a perfect identity mesh with a uniform density: e_adp == 1 everywhere
     ax = grid.axes()
     x = np.meshgrid(*ax, indexing="ij")
