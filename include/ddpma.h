@@ -51,7 +51,10 @@ enum { DDPMA_MON_UNIFORM = 0, DDPMA_MON_RING = 1, DDPMA_MON_MIXTURE = 2,
        /* arc-length monitors of the analytic test functions
         * (arc_length_monitor monitor.py:88-97, registry :223-345): u-backed */
        DDPMA_MON_BURGERS2D = 3, DDPMA_MON_SPIRAL2D = 4, DDPMA_MON_SPHERE3D = 5,
-       DDPMA_MON_NINE_SPHERES3D = 6, DDPMA_MON_QUASI1D_LINEAR = 7 };
+       DDPMA_MON_NINE_SPHERES3D = 6, DDPMA_MON_QUASI1D_LINEAR = 7,
+       /* arc-length monitor of a SampledField (monitor.py:361-391): u and
+        * grad u by multilinear interpolation of the lattice arrays */
+       DDPMA_MON_SAMPLED = 8 };
 
 /* CompGrid (grid.py:24-55). extents[k] = {a_k, b_k}; counts[k] = N_k.
  * explicit_geom = 1 describes one BoxGeometry (grid.py:261-307) instead of a
@@ -111,6 +114,14 @@ typedef struct {
                         solver's density is the pull-back of u); 0 = the
                         analytic raw at the clamped mesh points (e.g. after
                         normalize(), which drops u_fn, monitor.py:147-148) */
+  /* SAMPLED: lattice of lat[k] nodes per axis (host arrays, copied by the
+   * library): axes[k] (ascending), values (C order, already smoothed as the
+   * SampledField constructor does) and grads[k] = np.gradient(values, h_k,
+   * axis=k, edge_order=2) (monitor.py:372-380). */
+  int lat[3];
+  const double* axes[3];
+  const double* values;
+  const double* grads[3];
 } ddpma_monitor;
 
 /* normalize's probe quadrature (_trapezoid_mass, monitor.py:112-120) on the

@@ -692,6 +692,38 @@ class ArcLength:
         return np.sqrt(1.0 + np.sum(g * g, axis=-1))
 
 
+class Sampled:
+    """ddmesh/monitor.py:361-392 (SampledField) as an arc-length monitor:
+    u / grad u by scipy's RegularGridInterpolator(linear) of the (smoothed)
+    lattice and its np.gradient lattices; ``__call__`` is the arc length."""
+
+    def __init__(self, axes, values, smooth_passes=0):
+        from scipy.interpolate import RegularGridInterpolator as RGI
+        self.axes = tuple(np.asarray(a, dtype=float) for a in axes)
+        values = np.asarray(values, dtype=float)
+        if smooth_passes:
+            values = smooth(values, smooth_passes)
+        self.values = values
+        self.domain = tuple((float(a[0]), float(a[-1])) for a in self.axes)
+        hs = [float(a[1] - a[0]) for a in self.axes]
+        grads = [np.gradient(values, h, axis=k, edge_order=2) for k, h in enumerate(hs)]
+        self._iu = RGI(self.axes, values, method="linear")
+        self._ig = [RGI(self.axes, g, method="linear") for g in grads]
+
+    def u(self, p):
+        p = np.asarray(p, dtype=float)
+        return self._iu(p.reshape(-1, len(self.axes))).reshape(p.shape[:-1])
+
+    def gradient(self, p):
+        p = np.asarray(p, dtype=float)
+        flat = p.reshape(-1, len(self.axes))
+        return np.stack([g(flat) for g in self._ig], axis=-1).reshape(p.shape)
+
+    def __call__(self, p):
+        g = self.gradient(p)
+        return np.sqrt(1.0 + np.sum(g * g, axis=-1))
+
+
 def _pullback_gradient_sq(gxi, jac):
     """ddmesh/monitor.py:183-216."""
     dim = len(gxi)

@@ -16,12 +16,14 @@ from .grid import (INTERFACE, PHYSICAL, BoxGeometry, CompGrid, Decomposition,
 from .integrate import IntegrationWindow, rkc_coeffs
 from .monitor import (ArcLengthDensity, MixtureDensity, MonitorField, RingDensity,
                       ShellDensity, TestFunction, UniformDensity, arc_length_monitor,
-                      density_monitor, normalize, seeded_mixture,
+                      density_monitor, normalize, SampledField,
+                      sampled_field_from_csv, sampled_field_from_vtk, seeded_mixture,
                       test_function_registry)
 from .schwarz import (PhysicalMesh, SolverConfig, SolveResult, WindowRecord,
                       residual, solve, solve_single_domain)
 from .fileio import (read_mesh_vtk, read_scalar_field_vtk, write_field_csv, write_mesh_vtk,
                      write_scalar_field_vtk)
+from .pma import pma_rhs
 from .metrics import (ErrorReport, QualityReport, quality_measure, relative_errors,
                       restrict_to_grid)
 
@@ -33,9 +35,10 @@ __all__ = [
     "MonitorField", "density_monitor", "UniformDensity", "RingDensity",
     "ShellDensity", "MixtureDensity", "seeded_mixture",
     "TestFunction", "ArcLengthDensity", "arc_length_monitor", "test_function_registry", "normalize",
+    "SampledField", "sampled_field_from_csv", "sampled_field_from_vtk",
     "IntegrationWindow", "rkc_coeffs",
     "SolverConfig", "SolveResult", "WindowRecord", "PhysicalMesh",
-    "solve", "solve_single_domain", "residual",
+    "solve", "solve_single_domain", "residual", "pma_rhs",
     "DdmeshError", "ConfigurationError", "DomainError", "InvalidMonitorError",
     "MeshFileError", "StiffnessError",
     "write_mesh_vtk", "write_scalar_field_vtk", "write_field_csv", "read_mesh_vtk",

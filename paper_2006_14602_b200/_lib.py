@@ -26,6 +26,7 @@ STOP_MIN, STOP_MAX = 0, 1
 SCHEME_ADAPTIVE, SCHEME_EULER = 0, 1
 MON_UNIFORM, MON_RING, MON_MIXTURE = 0, 1, 2
 MON_BURGERS2D, MON_SPIRAL2D, MON_SPHERE3D, MON_NINE_SPHERES3D, MON_QUASI1D_LINEAR = 3, 4, 5, 6, 7
+MON_SAMPLED = 8
 NCLASS = 7
 
 
@@ -48,7 +49,9 @@ class Monitor(C.Structure):
                 ("amp", C.c_double), ("sharp", C.c_double), ("r2", C.c_double),
                 ("nbumps", C.c_int), ("c", C.POINTER(C.c_double)),
                 ("s", C.POINTER(C.c_double)), ("a", C.POINTER(C.c_double)),
-                ("eps", C.c_double), ("u_backed", C.c_int)]
+                ("eps", C.c_double), ("u_backed", C.c_int),
+                ("lat", C.c_int * 3), ("axes", C.POINTER(C.c_double) * 3),
+                ("values", C.POINTER(C.c_double)), ("grads", C.POINTER(C.c_double) * 3)]
 
 
 class SolverCfg(C.Structure):

@@ -62,6 +62,11 @@ struct MonitorD {
   double center[3];
   double amp, nsharp, r2;   // nsharp = -sharp
   double eps;               // burgers2d
+  // sampled field (kind 8): device copies of the lattice
+  int sm[3];
+  const double* sax[3];
+  const double* sv;
+  const double* sg[3];
   double c[MAXB * 3];
   double den[MAXB];         // (2.0*s)*s
   double a[MAXB];

@@ -125,6 +125,7 @@ struct ddpma_plan {
   MonitorD mon{};
   MonitorD* d_mon = nullptr;
   bool u_backed = false;   // arc-length monitor carrying u (pull-back density)
+  std::vector<void*> lat_allocs;   // sampled-field lattice copies
   long long arena = 0;
   double* d_arena = nullptr;
   Fields F{};
@@ -310,6 +311,39 @@ void fill_monitor(const ddpma_monitor* monitor, int dim, MonitorD& M) {
     M.den[b] = 2.0 * monitor->s[b] * monitor->s[b];
     M.a[b] = monitor->a[b];
   }
+}
+
+// Device copies of a sampled field's lattice (axes, values, gradients).
+cudaError_t upload_lattice(const ddpma_monitor* m, int dim, MonitorD& M,
+                           std::vector<void*>& owned) {
+  if (m->kind != DDPMA_MON_SAMPLED) return cudaSuccess;
+  size_t nv = 1;
+  for (int k = 0; k < dim; ++k) {
+    M.sm[k] = m->lat[k];
+    nv *= (size_t)m->lat[k];
+  }
+  auto up = [&](const double* src, size_t n, const double** dst) -> cudaError_t {
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc((void**)&d, sizeof(double) * n);
+    if (e != cudaSuccess) return e;
+    owned.push_back(d);
+    *dst = d;
+    return cudaMemcpy(d, src, sizeof(double) * n, cudaMemcpyHostToDevice);
+  };
+  cudaError_t e;
+  for (int k = 0; k < dim; ++k) {
+    if ((e = up(m->axes[k], (size_t)m->lat[k], &M.sax[k])) != cudaSuccess) return e;
+    if ((e = up(m->grads[k], nv, &M.sg[k])) != cudaSuccess) return e;
+  }
+  return up(m->values, nv, &M.sv);
+}
+
+bool sampled_ok(const ddpma_monitor* m, int dim) {
+  if (m->kind != DDPMA_MON_SAMPLED) return true;
+  if (!m->values) return false;
+  for (int k = 0; k < dim; ++k)
+    if (m->lat[k] < 2 || !m->axes[k] || !m->grads[k]) return false;
+  return true;
 }
 
 // u-backed monitors (arc-length of a test function): mesh_density is the
@@ -1223,6 +1257,7 @@ extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   cudaFree(p->d_arena);
   cudaFree(p->d_geo);
   cudaFree(p->d_mon);
+  for (void* q : p->lat_allocs) cudaFree(q);
   cudaFree(p->d_res);
   cudaFree(p->d_part);
   cudaFree(p->d_part2);
@@ -1283,11 +1318,15 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     set_global_error("mixture monitor supports at most 64 bumps");
     return DDPMA_ERR_CONFIG;
   }
-  if (monitor->kind < DDPMA_MON_UNIFORM || monitor->kind > DDPMA_MON_QUASI1D_LINEAR) {
+  if (monitor->kind < DDPMA_MON_UNIFORM || monitor->kind > DDPMA_MON_SAMPLED) {
     set_global_error("unknown monitor kind");
     return DDPMA_ERR_CONFIG;
   }
-  if (monitor->kind >= DDPMA_MON_BURGERS2D) {   // test-function domains (monitor.py:223-345)
+  if (!sampled_ok(monitor, grid->dim)) {
+    set_global_error("sampled field needs >= 2 lattice nodes per axis and its arrays");
+    return DDPMA_ERR_CONFIG;
+  }
+  if (monitor->kind >= DDPMA_MON_BURGERS2D && monitor->kind != DDPMA_MON_SAMPLED) {   // test-function domains (monitor.py:223-345)
     const bool three = monitor->kind == DDPMA_MON_SPHERE3D || monitor->kind == DDPMA_MON_NINE_SPHERES3D;
     if (grid->dim != (three ? 3 : 2)) {
       set_global_error("grid dimension does not match monitor domain");
@@ -1449,6 +1488,8 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   if ((ce = cudaMemcpy(p->d_geo, p->geo.data(), sizeof(SubGeo) * p->geo.size(),
                        cudaMemcpyHostToDevice)) != cudaSuccess)
     return fail(ce, "geo copy");
+  if ((ce = upload_lattice(monitor, p->dim, p->mon, p->lat_allocs)) != cudaSuccess)
+    return fail(ce, "sampled lattice");
   if ((ce = cudaMalloc((void**)&p->d_mon, sizeof(MonitorD))) != cudaSuccess) return fail(ce, "mon");
   if ((ce = cudaMemcpy(p->d_mon, &p->mon, sizeof(MonitorD), cudaMemcpyHostToDevice)) != cudaSuccess)
     return fail(ce, "mon copy");
@@ -2160,7 +2201,17 @@ extern "C" ddpma_status ddpma_monitor_mass(const ddpma_monitor* monitor, const i
     set_global_error("cudaSetDevice failed");
     return DDPMA_ERR_CUDA;
   }
+  if (!sampled_ok(monitor, dim)) {
+    set_global_error("sampled field needs >= 2 lattice nodes per axis and its arrays");
+    return DDPMA_ERR_CONFIG;
+  }
   const int nb = (int)((m.nodes + NT - 1) / NT);
+  std::vector<void*> lat;
+  if (upload_lattice(monitor, dim, M, lat) != cudaSuccess) {
+    for (void* q : lat) cudaFree(q);
+    set_global_error("CUDA error uploading the sampled lattice");
+    return DDPMA_ERR_CUDA;
+  }
   MonitorD* dm = nullptr;
   double *part = nullptr, *out = nullptr;
   ddpma_status s = DDPMA_OK;
@@ -2179,6 +2230,7 @@ extern "C" ddpma_status ddpma_monitor_mass(const ddpma_monitor* monitor, const i
   cudaFree(dm);
   cudaFree(part);
   cudaFree(out);
+  for (void* q : lat) cudaFree(q);
   if (s != DDPMA_OK) {
     set_global_error("CUDA error in ddpma_monitor_mass");
     return s;

@@ -263,13 +263,107 @@ def test_function_registry(name: str, **params) -> TestFunction:
 test_function_registry.__test__ = False   # not a pytest function
 
 
-def arc_length_monitor(source: TestFunction) -> MonitorField:
-    """Unnormalised arc-length density of ``source`` (monitor.py:88-97); u-backed,
-    so the solver's nodal density is the mesh pull-back of u (mesh_density)."""
+# ------------------------------------------------------ sampled fields --
+
+def _smooth(values: np.ndarray, passes: int) -> np.ndarray:
+    """Per-axis [1, 2, 1]/4 averaging with reflected edges (monitor.py:395-409)."""
+    out = values
+    for _ in range(passes):
+        for axis in range(out.ndim):
+            n = out.shape[axis]
+            left = np.take(out, [1] + list(range(0, n - 1)), axis=axis)
+            right = np.take(out, list(range(1, n)) + [n - 2], axis=axis)
+            out = 0.25 * left + 0.5 * out + 0.25 * right
+    return out
+
+
+class SampledField:
+    """Scalar u sampled on a lattice over a physical box (monitor.py:361-392).
+
+    Construction (smoothing, central-difference gradient lattices) is the
+    reference's one-time numpy preprocessing; the solver's per-window
+    interpolation of u and grad u at the mesh nodes runs on the device
+    (``DDPMA_MON_SAMPLED``).  ``u`` / ``gradient`` here are the host-side
+    API evaluations the reference class offers (scipy linear interpolation),
+    never called by ``solve``."""
+
+    def __init__(self, axes, values, smooth_passes: int = 0):
+        self.axes = tuple(np.ascontiguousarray(ax, dtype=np.float64) for ax in axes)
+        values = np.asarray(values, dtype=float)
+        if values.shape != tuple(len(ax) for ax in self.axes):
+            raise ConfigurationError("sample array shape does not match axes")
+        if smooth_passes:
+            values = _smooth(values, smooth_passes)
+        self.values = np.ascontiguousarray(values)
+        self.domain: Extents = tuple((float(ax[0]), float(ax[-1])) for ax in self.axes)
+        spacing = [float(ax[1] - ax[0]) for ax in self.axes]
+        self.grads = tuple(np.ascontiguousarray(np.gradient(self.values, h, axis=k, edge_order=2))
+                           for k, h in enumerate(spacing))
+
+    def _interp(self, field_values, points):
+        from scipy.interpolate import RegularGridInterpolator
+        points = np.asarray(points, dtype=float)
+        it = RegularGridInterpolator(self.axes, field_values, method="linear")
+        return it(points.reshape(-1, len(self.axes))).reshape(points.shape[:-1])
+
+    def u(self, points):
+        return self._interp(self.values, points)
+
+    def gradient(self, points):
+        return np.stack([self._interp(g, points) for g in self.grads], axis=-1)
+
+
+@dataclass(frozen=True, eq=False)
+class SampledArcLength:
+    """raw = sqrt(1 + |grad u|^2) of a SampledField (device kind 8)."""
+    field: SampledField
+
+    def __call__(self, p):
+        g = self.field.gradient(p)
+        return np.sqrt(1.0 + np.sum(g * g, axis=-1))
+
+
+def sampled_field_from_csv(path: str, smooth_passes: int = 0) -> SampledField:
+    """``x,y[,z],u`` rows covering a full uniform lattice (monitor.py:412-437)."""
+    rows = np.loadtxt(path, delimiter=",", comments="#", ndmin=2)
+    if rows.shape[1] not in (3, 4):
+        raise ConfigurationError(
+            f"{path}: expected 3 or 4 columns (x,y[,z],u), got {rows.shape[1]}")
+    dim = rows.shape[1] - 1
+    coords, u = rows[:, :dim], rows[:, dim]
+    axes = []
+    for k in range(dim):
+        ax = np.unique(coords[:, k])
+        if len(ax) < 3:
+            raise ConfigurationError(f"{path}: axis {k} has fewer than 3 levels")
+        steps = np.diff(ax)
+        if not np.allclose(steps, steps[0], rtol=1e-9, atol=1e-12):
+            raise ConfigurationError(f"{path}: axis {k} is not uniformly spaced")
+        axes.append(ax)
+    shape = tuple(len(ax) for ax in axes)
+    if rows.shape[0] != int(np.prod(shape)):
+        raise ConfigurationError(f"{path}: {rows.shape[0]} rows do not fill a {shape} lattice")
+    order = np.lexsort([coords[:, k] for k in reversed(range(dim))])
+    return SampledField(tuple(axes), u[order].reshape(shape), smooth_passes=smooth_passes)
+
+
+def sampled_field_from_vtk(path: str, smooth_passes: int = 0) -> SampledField:
+    """Scalar field in the package's structured-grid VTK format (monitor.py:440-444)."""
+    from . import fileio
+    axes, values = fileio.read_scalar_field_vtk(path)
+    return SampledField(axes, values, smooth_passes=smooth_passes)
+
+
+def arc_length_monitor(source) -> MonitorField:
+    """Unnormalised arc-length density of ``source`` (monitor.py:88-97): a
+    registered analytic TestFunction or a SampledField; u-backed, so the
+    solver's nodal density is the mesh pull-back of u (mesh_density)."""
+    if isinstance(source, SampledField):
+        return MonitorField(raw=SampledArcLength(source), domain=source.domain, u_fn=source.u)
     if not isinstance(source, TestFunction) or not isinstance(source.u, _TfU):
         raise ConfigurationError(
             "the device path supports arc-length monitors of the registered analytic "
-            "test functions (test_function_registry); sampled fields are not supported")
+            "test functions (test_function_registry) and of SampledField")
     return MonitorField(raw=ArcLengthDensity(source.u.name, source.u.eps),
                         domain=source.domain, u_fn=source.u)
 
@@ -285,8 +379,9 @@ def lower_monitor(mon: MonitorField, dim: int) -> NativeMonitor:
     """MonitorField -> ddpma_monitor, or ConfigurationError (no CPU fallback)."""
     if not isinstance(mon, MonitorField):
         raise ConfigurationError("monitor must be a MonitorField")
-    if mon.u_fn is not None and not (isinstance(mon.raw, ArcLengthDensity)
-                                     and mon.u_fn == _TfU(mon.raw.name, mon.raw.eps)):
+    if mon.u_fn is not None and not (
+            (isinstance(mon.raw, ArcLengthDensity) and mon.u_fn == _TfU(mon.raw.name, mon.raw.eps))
+            or (isinstance(mon.raw, SampledArcLength) and mon.u_fn == mon.raw.field.u)):
         raise ConfigurationError(
             "monitors backed by a physical scalar u are supported for the registered "
             "analytic test functions (arc_length_monitor); sampled fields are not")
@@ -317,6 +412,18 @@ def lower_monitor(mon: MonitorField, dim: int) -> NativeMonitor:
         d.u_backed = 1 if mon.u_fn is not None else 0
         if len(_DOMAINS[raw.name]) != dim:
             raise ConfigurationError("grid dimension does not match monitor domain")
+    elif isinstance(raw, SampledArcLength):
+        fld = raw.field
+        if len(fld.axes) != dim:
+            raise ConfigurationError("grid dimension does not match monitor domain")
+        d.kind = _lib.MON_SAMPLED
+        d.u_backed = 1 if mon.u_fn is not None else 0
+        for k, ax in enumerate(fld.axes):
+            d.lat[k] = len(ax)
+            d.axes[k] = _lib.dptr(ax)
+            d.grads[k] = _lib.dptr(fld.grads[k])
+        d.values = _lib.dptr(fld.values)
+        keep = [fld]
     elif isinstance(raw, MixtureDensity):
         c = np.ascontiguousarray(np.array(raw.c, dtype=np.float64).reshape(-1, dim))
         s = np.ascontiguousarray(np.array(raw.s, dtype=np.float64))

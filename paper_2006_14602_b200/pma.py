@@ -65,3 +65,21 @@ def mesh_density(mon: MonitorField, psi: np.ndarray, geom: BoxGeometry) -> np.nd
     density-only monitors), evaluated on the device."""
     with _plan(geom, mon=mon) as p:
         return p.raw_density(0, psi)
+
+
+def pma_rhs(psi: np.ndarray, monitor: MonitorField, geom: BoxGeometry,
+            det_floor: float = DET_FLOOR,
+            dirichlet_mask: np.ndarray | None = None) -> RhsEval:
+    """Moving-point right-hand side (pma.py:152-183): the monitor evaluated at
+    the clamped mesh points of ``psi`` (``eval_clamped``: analytic raw over the
+    normaliser, never the u pull-back) with the guard from ``max_value``.
+    Exported by the reference but unused by its ``solve`` (SURVEY §8(a) a21);
+    here a composition of the device mesh-density and frozen-RHS kernels."""
+    if dirichlet_mask is not None and not np.array_equal(dirichlet_mask, geom.dirichlet_mask()):
+        from .errors import ConfigurationError
+        raise ConfigurationError("custom dirichlet masks are not supported on the device path")
+    analytic = MonitorField(raw=monitor.raw, domain=monitor.domain)
+    with _plan(geom, det_floor, analytic) as p:
+        rho = p.raw_density(0, psi) / monitor.normalizer
+        f, flag = p.rhs_frozen(0, psi, rho, getattr(monitor, "max_value", None))
+    return RhsEval(f, flag)

@@ -86,6 +86,12 @@ def main():
         out[f"op_{name}_analytic"] = mon.raw(mon.clamp(mesh.coords))
         out[f"op_{name}_u"] = mon.u_fn(mon.clamp(mesh.coords))
         out[f"op_{name}_pull"] = rmon.mesh_density(mon, mesh.coords, geom.spacing)
+        # moving-point pma_rhs (pma.py:152-183) with the normalised monitor
+        nmon = rmon.normalize(mon, g)
+        ev = rpma.pma_rhs(psi, nmon, geom)
+        out[f"op_{name}_pmarhs"] = ev.values
+        out[f"op_{name}_pmarhs_flag"] = np.array(ev.det_clamped)
+        out[f"op_{name}_norm"] = np.array([nmon.normalizer, nmon.max_value])
         print("op", name, psi.shape)
     for name, params, counts in NORM_CASES:
         tf = rmon.test_function_registry(name, **params)

@@ -229,3 +229,37 @@ def test_device_quality_arc(sample, gold):
     assert err <= 1e-12
     assert abs(rep.e2 - e2) <= 1e-12 * abs(e2)
     assert rep.tangled == tangled
+
+
+@pytest.mark.parametrize("case", OP_CASES, ids=[c[0] for c in OP_CASES])
+def test_oracle_pma_rhs_bitwise(case, gold):
+    """Moving-point pma_rhs (pma.py:152-183) = the frozen RHS with
+    rho = raw(clamp(grad psi)) / normaliser and the max_value guard."""
+    name, params, dim, counts, layout, ov = case
+    mon, geom = _oracle_box(name, params, dim, counts, layout, ov, int(gold[f"op_{name}_sub"]))
+    psi = gold[f"op_{name}_psi"]
+    z, mx = gold[f"op_{name}_norm"]
+    coords, _ = O.mesh_of(psi, geom)
+    rho = mon(O.clamp(coords, mon.domain)) / z
+    f, flag = O.rhs_frozen(psi, rho, geom, O.DET_FLOOR, geom.mask(), mx)
+    assert np.array_equal(f, gold[f"op_{name}_pmarhs"])
+    assert flag == bool(gold[f"op_{name}_pmarhs_flag"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", OP_CASES, ids=[c[0] for c in OP_CASES])
+def test_device_pma_rhs(case, gold):
+    name, params, dim, counts, layout, ov = case
+    tf = P.test_function_registry(name, **params)
+    z, mx = gold[f"op_{name}_norm"]
+    mon = P.MonitorField(raw=P.arc_length_monitor(tf).raw, domain=tf.domain, normalizer=float(z),
+                         max_value=float(mx))
+    g = P.build_grid(dim, tf.domain, counts)
+    d = P.build_decomposition(g, layout, ov)
+    geom = P.subdomain_geometry(g, d.subdomains[int(gold[f"op_{name}_sub"])])
+    ev = P.pma_rhs(gold[f"op_{name}_psi"], mon, geom)
+    ref = gold[f"op_{name}_pmarhs"]
+    err = float(np.max(np.abs(ev.values - ref)))
+    print(f"[arc] pma_rhs {name}: max abs err {err:.3g}")
+    assert err <= 1e-12 * max(1.0, float(np.max(np.abs(ref))))
+    assert ev.det_clamped == bool(gold[f"op_{name}_pmarhs_flag"])
