@@ -3,6 +3,7 @@
 # threshold of the persistent window scheduler (plan.cu), single-role vs
 # warp-specialised 2D kernel. One bench line per setting into gpurun_out/.
 set -u
+mkdir -p gpurun_out
 out=gpurun_out/sweep_knobs.jsonl
 : > "$out"
 run() {
