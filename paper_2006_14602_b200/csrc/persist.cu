@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A
 // 2D window kernel with a chunked, double-buffered cp.async item pipeline.
 //
 // A CTA claims a CHUNK of consecutive work items of one subdomain action
-// (4 items while many subdomains are active, 1 on the tail's critical path),
+// (A.chunk_bulk = 8 items while many subdomains are active, A.chunk_tail = 2 on the tail's critical path),
 // then streams each item's sources into shared memory with 16-byte cp.async
 // (no register staging): the Y halo sources (y and the stage increment / f0 /
 // v tile, 34 x 36 each) and the centre fields the epilogue needs (|Omega|rho,
@@ -1752,7 +1752,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
   unsigned backoff = 32;
   while (true) {
     if (threadIdx.y == 0) {
-      // chunk of 4 items while many subdomains are active, 1 on the tail
+      // chunk of A.chunk_bulk items while many subdomains are active, A.chunk_tail on the tail
       const unsigned nd = *(volatile unsigned*)A.n_done;
       const int chunk = (A.nact - (int)nd) >= A.tail_n ? A.chunk_bulk : A.chunk_tail;
       int got, it0, nit;
