@@ -42,9 +42,9 @@ NCU_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
 
 # Kernel classes of the plan's profiler (ddpma.h): 0 = the fused eval kernel
 # (RKC2 stages, final evals, f0, power iteration; algorithmic bytes per
-# node-update from SURVEY §8(d): 48 B for a stage j>=4), 5 = mesh/density,
-# 6 = other (prologue, traces).
-CLASS_NAMES = ["eval", "unused1", "unused2", "unused3", "unused4", "mesh_density", "other"]
+# node-update from SURVEY §8(d): 48 B for a stage j>=4), 1 = mesh/density,
+# 2 = other (prologue, traces).
+CLASS_NAMES = ["eval", "mesh_density", "other"]
 
 
 def parse():

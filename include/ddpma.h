@@ -271,6 +271,18 @@ ddpma_status ddpma_apply_traces(ddpma_plan* plan, const double* recv_dev);
  * EulerIntegrator.advance :63-74). */
 ddpma_status ddpma_advance(ddpma_plan* plan);
 
+/* The integrator protocol (integrate.py:253-262, make_integrator(window)
+ * .advance(y, rhs_fn)) for the frozen-density PMA right-hand side that
+ * schwarz._advance_state builds (schwarz.py:201-208): advance the host box
+ * field `y` (in/out) of subdomain `sub_id` by one window of cfg.dtau with
+ * the plan's scheme, frozen nodal density `rho_host` and guard from
+ * `rho_max` (0 = no guard, pma.py:188-190).  The integrator caches (sigma,
+ * step size, refresh cadence; integrate.py:118-123) persist across calls on
+ * the same plan, as they persist across advance() calls of one
+ * Rkc2Integrator.  Errors: STIFFNESS (ddpma_error_info), VALUE/OVERFLOW. */
+ddpma_status ddpma_integrate_window(ddpma_plan* plan, int sub_id, double* y_host,
+                                   const double* rho_host, double rho_max);
+
 /* ------------------------------------------------ operator-level exports ---
  * Box-level operators on host arrays for parity tests and the public
  * operator API (pma.py).  `sub_id` selects the box geometry (face kinds,
@@ -319,10 +331,16 @@ ddpma_status ddpma_relative_errors(ddpma_plan* plan, int sub_id, const double* p
 ddpma_status ddpma_counters(const ddpma_plan* plan, int64_t* node_updates,
                             int64_t* rhs_evals, int64_t* launches,
                             double* algo_bytes);
+/* RHS evaluations per LOCAL subdomain (ascending global id) since the last
+ * ddpma_set_state: the device controller's tally of Rkc2Integrator /
+ * EulerIntegrator right-hand-side calls (integrate.py:163-250), i.e. the
+ * adaptive decision sequence of each subdomain.  Used by the parity tests
+ * and by the multi-GPU load balancer.  Writes min(n, nlocal) entries. */
+ddpma_status ddpma_sub_evals(const ddpma_plan* plan, int64_t* out, int n);
 /* Per-kernel-class device time (ms, CUDA events on the plan stream) when
- * profiling is enabled: class 0 = RKC stage (j>=4), 1 = stage 2/3,
- * 2 = final eval, 3 = f0/euler eval, 4 = power eval, 5 = mesh/density,
- * 6 = other.  bytes/launches per class likewise. */
+ * profiling is enabled: class 0 = evaluation kernels (the persistent window
+ * kernel), 1 = mesh/density pass, 2 = other (prologue, traces).
+ * bytes/launches per class likewise. */
 ddpma_status ddpma_set_profiling(ddpma_plan* plan, int on);
 ddpma_status ddpma_profile(const ddpma_plan* plan, double* ms, double* bytes,
                            int64_t* launches, int64_t* node_updates, int nclass);

@@ -27,7 +27,7 @@ SCHEME_ADAPTIVE, SCHEME_EULER = 0, 1
 MON_UNIFORM, MON_RING, MON_MIXTURE = 0, 1, 2
 MON_BURGERS2D, MON_SPIRAL2D, MON_SPHERE3D, MON_NINE_SPHERES3D, MON_QUASI1D_LINEAR = 3, 4, 5, 6, 7
 MON_SAMPLED = 8
-NCLASS = 7
+NCLASS = 3   # profiling classes: 0 eval (window kernel), 1 mesh/density, 2 other
 
 
 class Grid(C.Structure):
@@ -101,6 +101,8 @@ SIGNATURES = {
     "ddpma_rkc_step": (C.c_int, [_P, C.c_int, _D, _D, C.c_double, C.c_double, C.c_int,
                                  _D, _D, _I, _I]),
     "ddpma_counters": (C.c_int, [_P, _I64, _I64, _I64, _D]),
+    "ddpma_integrate_window": (C.c_int, [_P, C.c_int, _D, _D, C.c_double]),
+    "ddpma_sub_evals": (C.c_int, [_P, _I64, C.c_int]),
     "ddpma_set_profiling": (C.c_int, [_P, C.c_int]),
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),
     "ddpma_stream": (C.c_void_p, [_P]),

@@ -24,7 +24,7 @@ constexpr int TX = 32;            // tile width along the contiguous axis
 constexpr int TY = 8;             // tile height along the next axis
 constexpr int NT = TX * TY;       // threads per CTA
 constexpr int MAXB = 64;          // max Gaussian-mixture bumps
-constexpr int NCLASS = 7;         // profiling kernel classes (ddpma.h)
+constexpr int NCLASS = 3;         // profiling kernel classes (ddpma.h): eval, mesh/density, other
 // ddpma.h status / scheme values usable in device code
 constexpr int DDPMA_ERR_STIFFNESS_D = 3;
 constexpr int DDPMA_ERR_VALUE_D = 6;

@@ -45,6 +45,10 @@ enum { R_START = 0, R_ACCEPT, R_REJECT };
 constexpr double kSqrtEps = 1.4901161193847656e-08;   // np.sqrt(np.finfo(float).eps)
 constexpr double kStab = 0.653;                       // integrate.py:36
 constexpr double kMinStep = 1e-14;                    // integrate.py:37
+// Low half of a finished subdomain's synchronisation word.  Far from 2^32 so
+// that stray claim increments (a claimer that scanned the word before the
+// publish) can never carry into the sequence half and make it claimable.
+constexpr unsigned long long kDoneLow = 0x80000000ull;
 
 // Shared-memory copy of the log table (filled at the start of k_windowP;
 // the table lookups are the fp64 log's only memory accesses).
@@ -669,7 +673,7 @@ __device__ void d_publish(const WinArgs& A, DevCtl& c, DevCtl* gc) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     __stcg(reinterpret_cast<long long*>(&gc->t_done), (long long)now);
-    atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+    atomicExch(&gc->word, (seq << 32) | kDoneLow);
     atomicAdd(A.n_done, 1u);
   }
 }
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A
           if (more) {
             atomicExch(&gc->word, seq << 32);
           } else {
-            atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+            atomicExch(&gc->word, (seq << 32) | kDoneLow);
             atomicAdd(A.n_done, 1u);
           }
         }
@@ -1361,7 +1365,7 @@ __device__ void decide(const WinArgs& A, int l, const SubGeo& g, double sum, Dev
     if (more) {
       atomicExch(&gc->word, seq << 32);
     } else {
-      atomicExch(&gc->word, (seq << 32) | 0xffffffffull);
+      atomicExch(&gc->word, (seq << 32) | kDoneLow);
       atomicAdd(A.n_done, 1u);
     }
   }
@@ -1766,6 +1770,10 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
           s_exit = *(volatile unsigned*)A.n_done >= (unsigned)A.nact;
         } else {
           __threadfence();   // acquire
+          // the previous action's data was written by other CTAs through the
+          // generic proxy; the TMA loads of this chunk read it through the
+          // async proxy (this thread issues them)
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
           s_act = load_act(A, got);
           if (A.probe && got == A.probe_sub && it0 + nit == A.geo[got].nitems) {
             unsigned long long now;   // LAST chunk of the action claimed
@@ -2042,6 +2050,7 @@ __global__ void __launch_bounds__(NTW, 3) k_windowW(const WinArgs A) {
       backoff = 32;
       if (lane == 0) {
         __threadfence();   // acquire: the action and the data of the previous action
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");   // generic writes -> TMA reads
         const Act t = load_act(A, got);
         s_cs[slot].t = t;
         s_cs[slot].it0 = it0;

@@ -191,9 +191,13 @@ struct ddpma_plan {
   unsigned int* d_trace_n = nullptr;
   int trace_cap = 0;
   int win_blocks = 0;
+  int chunk_bulk = 8, chunk_tail = 2, tail_n = 16;   // window scheduler knobs (parsed once)
+  unsigned long long* d_probe = nullptr;             // DDPMA_PROBE timestamps (debug)
   bool host_ctl = false;
+  bool integ_ready = false;                // ddpma_integrate_window: integrators initialised
   void* d_tmap = nullptr;                  // 2D TMA tensor maps (persist.cu issue2_tma)
   std::vector<long long> last_evals;       // per local subdomain, previous window
+  std::vector<long long> sub_evals;        // per local subdomain, RHS evaluations since set_state
   long long mode_nodes[9] = {0};
 };
 
@@ -451,6 +455,7 @@ ddpma_status issue(ddpma_plan* p, std::vector<Entry>& ents, int slot) {
     if (e.mode != M_NORM) {
       nodes += nn;
       p->rhs_evals += 1;
+      p->sub_evals[e.sub] += 1;
     }
     sums |= e.mode == M_POWER || e.mode == M_POWER_SEED || e.mode == M_NORM;
   }
@@ -854,16 +859,15 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   A.trace = p->d_trace;
   A.trace_n = p->d_trace_n;
   A.trace_cap = p->trace_cap;
-  A.chunk_bulk = getenv("DDPMA_CHUNK") ? atoi(getenv("DDPMA_CHUNK")) : 8;
-  A.chunk_tail = getenv("DDPMA_CHUNK_TAIL") ? atoi(getenv("DDPMA_CHUNK_TAIL")) : 2;  // profiles/r1_sweep_knobs*.jsonl: 2 beats 1 by ~1.2 %
-  A.tail_n = getenv("DDPMA_TAIL_N") ? atoi(getenv("DDPMA_TAIL_N")) : 16;
+  A.chunk_bulk = p->chunk_bulk;
+  A.chunk_tail = p->chunk_tail;
+  A.tail_n = p->tail_n;
   A.tmap = p->d_tmap;
-  static unsigned long long* d_probe = nullptr;
-  const char* pe = getenv("DDPMA_PROBE");
+  unsigned long long* d_probe = p->d_probe;
+  const bool pe = d_probe != nullptr;
   if (pe) {
     A.probe_cap = 1 << 16;
-    if (!d_probe) cudaMalloc((void**)&d_probe, sizeof(unsigned long long) * 4 * A.probe_cap);
-    cudaMemsetAsync(d_probe, 0, sizeof(unsigned long long) * 4 * A.probe_cap, p->st);
+    CK(p, cudaMemsetAsync(d_probe, 0, sizeof(unsigned long long) * 4 * A.probe_cap, p->st));
     A.probe = d_probe;
     A.probe_sub = order[0];
   }
@@ -892,6 +896,7 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
     bytes += c.bytes - prev.bytes;
     nodes += de * p->geo[l].nodes;
     p->rhs_evals += de;
+    p->sub_evals[l] += de;
     prev.evals = c.evals;
     prev.bytes = c.bytes;
     p->ctl[l].yi = c.yi;
@@ -919,7 +924,7 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   }
   if (pe) {
     std::vector<unsigned long long> pr(4 * (size_t)A.probe_cap);
-    cudaMemcpy(pr.data(), d_probe, sizeof(unsigned long long) * pr.size(), cudaMemcpyDeviceToHost);
+    CK(p, cudaMemcpy(pr.data(), d_probe, sizeof(unsigned long long) * pr.size(), cudaMemcpyDeviceToHost));
     double s_wait = 0, s_proc = 0, s_dec = 0;
     long n = 0;
     for (int i = 0; i < A.probe_cap; ++i) {
@@ -1006,9 +1011,9 @@ ddpma_status mesh_pass(ddpma_plan* p, bool with_res) {
   const long long nodes = entries_nodes(p, ents.data(), (int)ents.size());
   if (p->prof) {
     cudaEventRecord(e1, p->st);
-    p->prof_pending.push_back({e0, e1, 5, 24.0 * nodes, nodes});
+    p->prof_pending.push_back({e0, e1, 1, 24.0 * nodes, nodes});
   }
-  account(p, 5, nodes, with_res ? 24.0 : 16.0, false);
+  account(p, 1, nodes, with_res ? 24.0 : 16.0, false);
   launch_finalize((Entry*)d, (int)ents.size(), p->d_part, p->d_res, 0, p->st);
   launch_finalize((Entry*)d, (int)ents.size(), p->d_part2, p->d_res, 1, p->st);
   if ((s = check_launch(p, "mesh")) != DDPMA_OK) return s;
@@ -1056,7 +1061,7 @@ ddpma_status prologue(ddpma_plan* p, const std::vector<int>& act, double z) {
   a.ent = (Entry*)d;
   a.nent = (int)ents.size();
   launch_prologue(a, nb, z, p->st);
-  account(p, 6, entries_nodes(p, ents.data(), (int)ents.size()), 32.0, false);
+  account(p, 2, entries_nodes(p, ents.data(), (int)ents.size()), 32.0, false);
   p->have_old = true;
   return check_launch(p, "prologue");
 }
@@ -1135,7 +1140,7 @@ ddpma_status run_faces(ddpma_plan* p, std::vector<FaceJob>& jobs, int nnodes) {
   ddpma_status s;
   if ((s = stage_put(p, jobs.data(), jobs.size() * sizeof(FaceJob), &d)) != DDPMA_OK) return s;
   launch_faces((FaceJob*)d, (int)jobs.size(), nnodes, p->st);
-  account(p, 6, nnodes, 16.0, false);
+  account(p, 2, nnodes, 16.0, false);
   return check_launch(p, "faces");
 }
 
@@ -1283,6 +1288,7 @@ extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   cudaFree(p->d_ndone);
   cudaFree(p->d_trace);
   cudaFree(p->d_tmap);
+  cudaFree(p->d_probe);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->st) cudaStreamDestroy(p->st);
   delete p;
@@ -1314,6 +1320,24 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     set_global_error("euler mode needs at least 1 substep");
     return DDPMA_ERR_CONFIG;
   }
+  // window scheduler knobs (profiling sweeps): parsed once, validated
+  int knob[3] = {8, 2, 16};   // DDPMA_CHUNK, DDPMA_CHUNK_TAIL (r1 sweeps: 2 beats 1 by ~1.2 %), DDPMA_TAIL_N
+  {
+    const char* names[3] = {"DDPMA_CHUNK", "DDPMA_CHUNK_TAIL", "DDPMA_TAIL_N"};
+    const int hi[3] = {64, 64, 1 << 20};
+    for (int i = 0; i < 3; ++i) {
+      const char* v = getenv(names[i]);
+      if (!v) continue;
+      char* end = nullptr;
+      const long x = strtol(v, &end, 10);
+      if (end == v || *end != '\0' || x < 1 || x > hi[i]) {
+        set_global_error(std::string(names[i]) + " must be an integer in [1, " +
+                         std::to_string(hi[i]) + "], got '" + v + "'");
+        return DDPMA_ERR_CONFIG;
+      }
+      knob[i] = (int)x;
+    }
+  }
   if (monitor->kind == DDPMA_MON_MIXTURE && (monitor->nbumps < 0 || monitor->nbumps > MAXB)) {
     set_global_error("mixture monitor supports at most 64 bumps");
     return DDPMA_ERR_CONFIG;
@@ -1338,6 +1362,9 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     }
   }
   auto* p = new ddpma_plan();
+  p->chunk_bulk = knob[0];
+  p->chunk_tail = knob[1];
+  p->tail_n = knob[2];
   p->device = device;
   p->grid = *grid;
   p->cfg = *cfg;
@@ -1567,6 +1594,10 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
         return fail(ce, "trace");
     }
     p->win_blocks = window_blocks(p->dim, P.pow2);
+    if (getenv("DDPMA_PROBE")) {
+      if ((ce = cudaMalloc((void**)&p->d_probe, sizeof(unsigned long long) * 4 * (1 << 16))) != cudaSuccess)
+        return fail(ce, "probe");
+    }
     if (p->dim == 2 && getenv("DDPMA_NO_TMA") == nullptr) {
       // one 2D tensor map per (subdomain, field, box): halo box 36 x (IR2+2) at
       // (c0-2, r0-1), centre box 32 x IR2; out-of-box elements are zero-filled
@@ -1620,17 +1651,24 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   return DDPMA_OK;
 }
 
+// Fresh integrators for every local subdomain (schwarz.py:133,
+// integrate.py:118-123: no sigma / step caches yet).
+ddpma_status reset_integrators(ddpma_plan* p) {
+  for (auto& c : p->ctl) c = Ctl{};
+  const int nl = (int)p->local.size();
+  memset(p->h_ctl, 0, sizeof(DevCtl) * nl);
+  for (int l = 0; l < nl; ++l) p->h_ctl[l].interval = 25;   // _SIGMA_REFRESH
+  CK(p, cudaMemcpyAsync(p->d_ctl, p->h_ctl, sizeof(DevCtl) * nl, cudaMemcpyHostToDevice, p->st));
+  p->ctl_prev.assign(nl, DevCtl{});
+  p->last_evals.assign(nl, 0);
+  p->sub_evals.assign(nl, 0);
+  return DDPMA_OK;
+}
+
 extern "C" ddpma_status ddpma_set_state(ddpma_plan* p, const double* psi_global_host) {
   CK(p, cudaSetDevice(p->device));
-  for (auto& c : p->ctl) c = Ctl{};   // fresh integrators (schwarz.py:133)
-  {
-    const int nl = (int)p->local.size();
-    memset(p->h_ctl, 0, sizeof(DevCtl) * nl);
-    for (int l = 0; l < nl; ++l) p->h_ctl[l].interval = 25;   // _SIGMA_REFRESH
-    CK(p, cudaMemcpyAsync(p->d_ctl, p->h_ctl, sizeof(DevCtl) * nl, cudaMemcpyHostToDevice, p->st));
-    p->ctl_prev.assign(nl, DevCtl{});
-    p->last_evals.assign(nl, 0);
-  }
+  ddpma_status s0 = reset_integrators(p);
+  if (s0 != DDPMA_OK) return s0;
   int nb;
   std::vector<Entry> ents = all_entries(p, &nb);
   void* d;
@@ -2068,6 +2106,32 @@ extern "C" ddpma_status ddpma_rhs_frozen(ddpma_plan* p, int sub_id, const double
   return d2h_box(p, l, p->F.f[0], F_out);
 }
 
+extern "C" ddpma_status ddpma_integrate_window(ddpma_plan* p, int sub_id, double* y,
+                                               const double* rho, double rho_max) {
+  const int l = local_of_checked(p, sub_id);
+  if (l < 0) {
+    p->err = "subdomain is not local to this plan";
+    return DDPMA_ERR_STATE;
+  }
+  CK(p, cudaSetDevice(p->device));
+  ddpma_status s;
+  if (!p->integ_ready) {   // first advance() of this integrator: no caches
+    if ((s = reset_integrators(p)) != DDPMA_OK) return s;
+    p->integ_ready = true;
+  }
+  // y into the subdomain's current buffer (the device controller's yi),
+  // the frozen density into raw, measure*rho and the guard (pma.py:186-219)
+  if ((s = h2d_box(p, l, y, p->F.y[p->ctl[l].yi])) != DDPMA_OK) return s;
+  if ((s = h2d_box(p, l, rho, p->F.raw)) != DDPMA_OK) return s;
+  set_guard(p, rho_max);
+  std::vector<int> one{l};
+  if ((s = prologue(p, one, 1.0)) != DDPMA_OK) return s;   // mr = measure*(rho/1.0)
+  p->fail = Failure{};
+  if ((s = advance_set(p, one)) != DDPMA_OK) return s;
+  if (p->fail.set) return report_failure(p);
+  return d2h_box(p, l, p->F.y[p->ctl[l].yi], y);
+}
+
 extern "C" ddpma_status ddpma_mesh(ddpma_plan* p, int sub_id, const double* psi, double* coords,
                                    double* jac) {
   const int l = local_of_checked(p, sub_id);
@@ -2410,6 +2474,13 @@ extern "C" ddpma_status ddpma_counters(const ddpma_plan* p, int64_t* node_update
   if (rhs_evals) *rhs_evals = p->rhs_evals;
   if (launches) *launches = p->launches;
   if (algo_bytes) *algo_bytes = p->algo_bytes;
+  return DDPMA_OK;
+}
+
+extern "C" ddpma_status ddpma_sub_evals(const ddpma_plan* p, int64_t* out, int n) {
+  if (!p || (n > 0 && !out)) return DDPMA_ERR_STATE;
+  const int nl = (int)p->local.size();
+  for (int l = 0; l < n && l < nl; ++l) out[l] = l < (int)p->sub_evals.size() ? p->sub_evals[l] : 0;
   return DDPMA_OK;
 }
 

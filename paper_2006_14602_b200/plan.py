@@ -211,6 +211,14 @@ class Plan:
         return {"node_updates": nu.value, "rhs_evals": ev.value, "launches": la.value,
                 "algo_bytes": by.value}
 
+    def sub_evals(self) -> np.ndarray:
+        """RHS evaluations of every local subdomain since set_state (local
+        order = ascending global id): the controller's per-subdomain tally."""
+        out = np.zeros(len(self.local), dtype=np.int64)
+        self.check(self.L.ddpma_sub_evals(self.h, out.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          len(self.local)))
+        return out
+
     def set_profiling(self, on: bool):
         self.L.ddpma_set_profiling(self.h, 1 if on else 0)
 
@@ -317,6 +325,15 @@ class Plan:
                                          float(rho_max or 0.0), float(h), int(s), _lib.dptr(d),
                                          _lib.dptr(fnew), C.byref(fl), C.byref(ef)))
         return d, fnew, bool(fl.value), bool(ef.value)
+
+    def integrate_window(self, sub_id, y, rho, rho_max):
+        """One window of the plan's integrator on box field ``y`` (returned
+        as a new array) with a frozen nodal density (ddpma_integrate_window)."""
+        out = np.array(y, dtype=np.float64, order="C", copy=True)
+        rho = np.ascontiguousarray(np.broadcast_to(rho, out.shape), dtype=np.float64)
+        self.check(self.L.ddpma_integrate_window(self.h, int(sub_id), _lib.dptr(out),
+                                                 _lib.dptr(rho), float(rho_max or 0.0)))
+        return out
 
 
 __all__ = ["Plan", "PHYSICAL", "INTERFACE"]

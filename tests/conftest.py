@@ -1,16 +1,25 @@
 import os
 import sys
 
-import numpy as np
-import pytest
+# before numpy loads OpenBLAS: the oracle's sigma estimate uses BLAS dot
+# (np.linalg.norm), whose threaded summation order would change its last bits
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+import pytest  # noqa: E402
+
+try:   # numpy may already have been imported (plugins): limit its BLAS pool too
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1, "blas")
+except Exception:  # pragma: no cover
+    pass
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(REPO, "tests", "golden")
 for p in (REPO, os.path.join(REPO, "oracle"), GOLDEN):
     if p not in sys.path:
         sys.path.insert(0, p)
-
-os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 
 
 def pytest_configure(config):

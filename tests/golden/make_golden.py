@@ -356,3 +356,130 @@ def gen_envelopes():
 if __name__ == "__main__" and "envelopes" in sys.argv[1:]:
     ONLY[:] = [w[5:] for w in sys.argv[1:] if w.startswith("only=")]
     gen_envelopes()
+
+
+# ------------------------------------------------- BASELINE-size windows ----
+# One full window of the C3 / C5 BASELINE configs (all 64 subdomains, parallel
+# transmission, reference defaults except a reduced window length so the
+# reference finishes on a CPU) — the configurations the bench runs.  Large
+# arrays are pinned by digests + sampled nodes; the per-subdomain RHS-call
+# counts pin the adaptive decision sequence of every subdomain.
+WINDOW_CASES = {
+    "C3": dict(dtau=1e-6),
+    "C5": dict(dtau=1e-5),
+}
+
+
+class CountRhsPerSub(CountRhs):
+    """CountRhs, bucketed by subdomain (keyed on the box origin)."""
+
+    def __enter__(self):
+        self.per = {}
+
+        def wrapped(psi, rho, geom, *a, **k):
+            key = tuple(float(ax[0]) for ax in geom.axes)
+            self.per[key] = self.per.get(key, 0) + 1
+            self.calls += 1
+            self.nodes += psi.size
+            return self.orig(psi, rho, geom, *a, **k)
+        rpma.pma_rhs_frozen = wrapped
+        return self
+
+
+def gen_windows(names=("C3", "C5"), workers=8):
+    for name in names:
+        kw = WINDOW_CASES[name]
+        rg, rd, mon = ref_case(name)
+        m = ddmesh.density_monitor(mon, rg.extents)
+        t0 = time.perf_counter()
+        with CountRhsPerSub() as c:
+            res = ddmesh.solve(rg, rd, m, cfg(max_windows=1, transmission="parallel",
+                                              workers=workers, **kw))
+        d = result_arrays(res, full=False, sample=True)
+        calls = []
+        for sub in rd.subdomains:
+            geom = ddmesh.subdomain_geometry(rg, sub)
+            calls.append(c.per[tuple(float(ax[0]) for ax in geom.axes)])
+        d["sub_rhs_calls"] = np.array(calls)
+        for i, sp in enumerate(res.sub_psi):
+            idx = R.sample_index(sp.shape, n=512, seed=11 + i)
+            d[f"sub{i}_idx"] = idx
+            d[f"sub{i}_smp"] = sp.reshape(-1)[idx]
+            d[f"sub{i}_sha"] = np.array(R.digest(sp))
+        d["rhs_calls"] = np.array(c.calls)
+        d["node_updates"] = np.array(c.nodes)
+        d["dtau"] = np.array(kw["dtau"])
+        d["seconds"] = np.array(time.perf_counter() - t0)
+        np.savez_compressed(os.path.join(HERE, f"win_{name}.npz"), **d)
+        print("window", name, f"{time.perf_counter() - t0:.1f}s", c.calls, c.nodes,
+              "res", float(np.max(d["residuals"])), "jmin", float(d["jac_min"][0]), flush=True)
+
+
+if __name__ == "__main__" and any(w.startswith("windows") for w in sys.argv[1:]):
+    sel = [w.split("=")[1] for w in sys.argv[1:] if w.startswith("windows=")]
+    gen_windows(tuple(sel) if sel else ("C3", "C5"))
+
+
+# ------------------------------------------------ deterministic prefixes ----
+# The default-profile C1 variants are chaotic over tens of windows (see the
+# envelopes), but their first windows precede the first positivity-flag
+# event and are deterministic to ulps: full coordinates after PREFIX_WINDOWS
+# windows pin them at 1e-10 (tests/test_gpu_parity.py::test_c1_prefix_coords).
+PREFIX_WINDOWS = 3
+
+
+def gen_prefix():
+    rg, rd, mon = ref_case("C1")
+    m1 = ddmesh.density_monitor(mon, rg.extents)
+    k = PREFIX_WINDOWS
+    init = R.perturbed_global(rg.axes())
+    rd4 = ddmesh.build_decomposition(rg, (4, 1), 3)
+    cases = {
+        "C1_parallel": lambda: ddmesh.solve(rg, rd, m1, cfg(max_windows=k, transmission="parallel")),
+        "C1_alternating": lambda: ddmesh.solve(rg, rd, m1, cfg(max_windows=k,
+                                                                transmission="alternating")),
+        "C1_single": lambda: ddmesh.solve_single_domain(rg, m1, cfg(max_windows=k)),
+        "C1_warm": lambda: ddmesh.solve(rg, rd, m1, cfg(max_windows=k, transmission="parallel"),
+                                        initial=init),
+        "C1_cap8": lambda: ddmesh.solve(rg, rd, m1, cfg(max_windows=k, transmission="alternating",
+                                                         max_stages=8)),
+        "C1_slab4": lambda: ddmesh.solve(rg, rd4, m1, cfg(max_windows=k, transmission="parallel")),
+    }
+    out = {}
+    for tag, fn in cases.items():
+        with CountRhs() as c:
+            res = fn()
+        out[tag + "_coords"] = res.mesh.coords
+        out[tag + "_psi"] = res.psi
+        out[tag + "_residuals"] = np.array([h.residuals for h in res.history])
+        out[tag + "_node_updates"] = np.array(c.nodes)
+        print("prefix", tag, c.calls, flush=True)
+    np.savez_compressed(os.path.join(HERE, f"prefix{k}_C1.npz"), **out)
+
+
+if __name__ == "__main__" and "prefix" in sys.argv[1:]:
+    gen_prefix()
+
+
+# ------------------------------------------------------ public API pins ----
+def gen_api():
+    """The reference's public names (ddmesh.__all__) and host-helper outputs."""
+    from ddmesh import metrics as rmet
+    names = sorted(ddmesh.__all__)
+    rg, rd, mon = ref_case("C1")
+    out = {"names": np.array(names)}
+    for sid in (0, 3):
+        geom = ddmesh.subdomain_geometry(rg, rd.subdomains[sid])
+        out[f"psi0_s{sid}"] = rpma.initial_potential(geom)
+    fit = rmet.convergence_slope([(1 / 16, 3.1e-3), (1 / 32, 8.2e-4), (1 / 64, 2.05e-4),
+                                  (1 / 128, 5.3e-5)])
+    out["slope"] = np.array([fit.slope, fit.intercept, fit.residual])
+    a = 0.7   # rho = 1 + a (2x - 1) on [0, 1], R(x) = x + a (x^2 - x)
+    out["quasi1d"] = rmet.quasi1d_oracle(lambda x: 1.0 + a * (2.0 * x - 1.0),
+                                         lambda x: x + a * (x * x - x), 33)
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
+    print("api", len(names))
+
+
+if __name__ == "__main__" and "api" in sys.argv[1:]:
+    gen_api()

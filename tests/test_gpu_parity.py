@@ -158,7 +158,12 @@ def check_run(res, gold, tag=None, coord_tol=COORD_TOL):
         spread_ok = dc <= 20.0 * float(env["coords"])
         print(f"[parity] {tag}: chaotic reference; prefix({k}) match={prefix_ok}, "
               f"max|dcoords|={dc:.3g} vs reference spread {float(env['coords']):.3g}")
-        assert prefix_ok or spread_ok
+        # the final mesh must lie within the reference's own one-ulp spread;
+        # C1 runs also have a deterministic prefix (coordinates of that
+        # prefix are pinned at 1e-10 by test_c1_prefix_coords)
+        assert spread_ok, (dc, float(env["coords"]))
+        if tag.startswith("C1"):
+            assert prefix_ok
         return
     n_ref = int(gold["node_updates"])
     n_rel = abs(res.stats["node_updates"] - n_ref) / n_ref
@@ -355,3 +360,152 @@ def test_c4_one_window():
     og, g, d, m, lay, raw = baseline("C4")
     res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=1, transmission="parallel"))
     check_run(res, golden("run_C4_parallel_1.npz"), "C4_parallel_1")
+
+
+# ------------------------------------------- BASELINE configs as benched ---
+
+@pytest.mark.parametrize("tr", ["parallel", "alternating"])
+def test_c1_reference_defaults_2000(tr):
+    """BASELINE config 1 literally: 65^2, 2x2, overlap 4, ring monitor, the
+    reference defaults, 2000 windows.  The reference converges there (final
+    residuals ~5e-17); the converged mesh is the steady state of the DD
+    iteration, so coordinates must agree to 1e-10 even though the transient
+    is chaotic at the ulp level (the node-update count is reported, not
+    pinned)."""
+    g, d, m = ring_case()
+    res = P.solve(g, d, m, P.SolverConfig(tol=1e-300, max_windows=2000, transmission=tr))
+    gold = golden(f"run_C1_{tr}_2000.npz")
+    assert res.windows == 2000
+    dc = float(np.max(np.abs(res.mesh.coords - gold["coords"])))
+    dp = res.psi - gold["psi"]
+    dpc = float(np.max(np.abs(dp - dp.mean())))
+    nrel = res.stats["node_updates"] / int(gold["node_updates"]) - 1.0
+    print(f"[parity] C1 defaults {tr} x2000: max|dcoords|={dc:.3g} max|dpsi-const|={dpc:.3g} "
+          f"final residual {res.final_residual:.3g} (ref {float(gold['final_residual']):.3g}) "
+          f"node-updates {res.stats['node_updates']} vs ref {int(gold['node_updates'])} ({nrel:+.3%})")
+    assert float(np.max(res.history[-1].residuals)) < 1e-12
+    assert dc <= COORD_TOL, dc
+    assert dpc <= COORD_TOL, dpc
+    assert np.max(np.abs(res.mesh.jac - gold["jac"])) <= 1e-8
+    for i, sp in enumerate(res.sub_psi):
+        ds = sp - gold[f"sub_psi{i}"] if f"sub_psi{i}" in gold else None
+        if ds is not None:
+            assert np.max(np.abs(ds - ds.mean())) <= COORD_TOL
+    assert abs(res.overlap_gap - float(gold["overlap_gap"])) <= 1e-10
+
+
+@pytest.mark.parametrize("tag", ["C1_parallel", "C1_alternating", "C1_single", "C1_warm",
+                                 "C1_cap8", "C1_slab4"])
+def test_c1_prefix_coords(tag):
+    """The default-profile C1 variants whose long runs are chaotic: their
+    first 3 windows are deterministic, so full coordinates and psi after 3
+    windows are pinned at 1e-10 against the reference (make_golden.py
+    gen_prefix), and so is the adaptive decision sequence (node-updates)."""
+    gold = golden("prefix3_C1.npz")
+    g, d, m = ring_case()
+    cfg = dict(tol=1e-300, max_windows=3)
+    initial = None
+    if tag == "C1_single":
+        res = P.solve_single_domain(g, m, P.SolverConfig(**cfg))
+    else:
+        if tag == "C1_slab4":
+            d = P.build_decomposition(g, (4, 1), 3)
+        if tag == "C1_warm":
+            initial = R.perturbed_global(g.axes())
+        cfg["transmission"] = "alternating" if tag in ("C1_alternating", "C1_cap8") else "parallel"
+        if tag == "C1_cap8":
+            cfg["max_stages"] = 8
+        res = P.solve(g, d, m, P.SolverConfig(**cfg), initial=initial)
+    dc = float(np.max(np.abs(res.mesh.coords - gold[tag + "_coords"])))
+    dp = res.psi - gold[tag + "_psi"]
+    dpc = float(np.max(np.abs(dp - dp.mean())))
+    print(f"[parity] {tag} prefix 3: max|dcoords|={dc:.3g} max|dpsi-const|={dpc:.3g}")
+    assert res.stats["node_updates"] == int(gold[tag + "_node_updates"])
+    assert rel_close(np.array([h.residuals for h in res.history]), gold[tag + "_residuals"], 1e-9)
+    assert dc <= COORD_TOL and dpc <= COORD_TOL
+
+
+def _window_case(name):
+    gold = golden(f"win_{name}.npz")
+    og, g, d, mon, lay, raw = baseline(name)
+    cfg = P.SolverConfig(tol=1e-300, max_windows=1, transmission="parallel",
+                         dtau=float(gold["dtau"]))
+    return gold, g, d, mon, cfg
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_baseline_window_parity(name):
+    """One full window of the benched BASELINE configs (all 64 subdomains,
+    reference defaults, reduced window length so the reference finishes on a
+    CPU; make_golden.py gen_windows).  Pins every subdomain's adaptive
+    decision sequence (RHS-evaluation count), the per-subdomain residuals,
+    and sampled coordinates / psi / sub_psi at 1e-10."""
+    gold, g, d, mon, cfg = _window_case(name)
+    res = P.solve(g, d, mon, cfg)
+    evals = np.asarray(res.stats["sub_rhs_evals"])
+    assert np.array_equal(evals, gold["sub_rhs_calls"]), (evals, gold["sub_rhs_calls"])
+    assert res.stats["node_updates"] == int(gold["node_updates"])
+    hr = np.array([h.residuals for h in res.history])
+    assert rel_close(hr, gold["residuals"], 1e-9)
+    flat = res.mesh.coords.reshape(res.psi.size, -1)[gold["coords_idx"]]
+    dc = float(np.max(np.abs(flat - gold["coords_smp"])))
+    dp = res.psi.reshape(-1)[gold["psi_idx"]] - gold["psi_smp"]
+    dpc = float(np.max(np.abs(dp - dp.mean())))
+    dsub = 0.0
+    for i, sp in enumerate(res.sub_psi):
+        ds = sp.reshape(-1)[gold[f"sub{i}_idx"]] - gold[f"sub{i}_smp"]
+        dsub = max(dsub, float(np.max(np.abs(ds))))
+    dj = float(np.max(np.abs(res.mesh.jac.reshape(-1)[gold["jac_idx"]] - gold["jac_smp"])
+                      / np.maximum(1.0, np.abs(gold["jac_smp"]))))
+    print(f"[parity] {name} window dtau={float(gold['dtau'])}: max|dcoords|={dc:.3g} "
+          f"max|dpsi-const|={dpc:.3g} max|dsub_psi|={dsub:.3g} jac rel {dj:.3g} "
+          f"jac_min {res.history[0].jac_min:.6g} (ref {float(gold['jac_min'][0]):.6g})")
+    assert dc <= COORD_TOL and dpc <= COORD_TOL and dsub <= COORD_TOL
+    assert rel_close([res.history[0].jac_min, res.history[0].jac_max],
+                     [float(gold["jac_min"][0]), float(gold["jac_max"][0])], 1e-6)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_baseline_rerun_bitwise(name):
+    """Two windows of C3 / C5 run twice: psi, Jacobian and every subdomain's
+    RHS-evaluation count bitwise identical (deterministic fixed-order
+    reductions, scheduling-independent results)."""
+    gold, g, d, mon, cfg = _window_case(name)
+    import dataclasses
+    cfg = dataclasses.replace(cfg, max_windows=2)
+    a = P.solve(g, d, mon, cfg)
+    b = P.solve(g, d, mon, cfg)
+    assert np.array_equal(a.stats["sub_rhs_evals"], b.stats["sub_rhs_evals"])
+    assert np.array_equal(a.psi, b.psi)
+    assert np.array_equal(a.mesh.jac, b.mesh.jac)
+    assert all(np.array_equal(x, y) for x, y in zip(a.sub_psi, b.sub_psi))
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_rkc_step_baseline_boxes(name):
+    """One RKC2 step (ddpma_rkc_step) on real C3 / C5 subdomain boxes (first,
+    interior, last) against the oracle's _rkc_step (integrate.py:163-178)."""
+    og, g, d, mon, lay, raw = baseline(name)
+    od = O.make_decomposition(og, lay, d.overlap)
+    steps = ((2e-9, 3), (1e-8, 9)) if name == "C3" else ((1e-7, 3), (5e-7, 5))
+    for sid in R.rhs_case_subs(lay):
+        geom = P.subdomain_geometry(g, d.subdomains[sid])
+        ogeom = O.box_geom(og, od.subs[sid])
+        y = R.perturbed_global(geom.axes)
+        coords = np.stack(O.coords_fd(y, ogeom), axis=-1)
+        rho = raw(np.clip(coords, 0.0, 1.0)) / R.RHS_Z
+        rmax = float(rho.max())
+        mask = ogeom.mask()
+        fn = lambda v: O.rhs_frozen(v, rho, ogeom, O.DET_FLOOR, mask, rmax)
+        f0, _ = fn(y)
+        integ = O.Rkc2(1e-3)
+        with Plan.for_geometry(geom, P.SolverConfig()) as p:
+            for h, s in steps:
+                od_, ofn, ofl, oend = integ._step(y, f0, h, s, fn)
+                dd, fnew, fl, end = p.rkc_step(0, y, rho, rmax, h, s)
+                assert (fl, end) == (ofl, oend), (name, sid, h, s)
+                # relative to the field's scale (d_s ~ h*F is small)
+                ed = float(np.max(np.abs(dd - od_))) / float(np.max(np.abs(od_)))
+                ef = float(np.max(np.abs(fnew - ofn))) / float(np.max(np.abs(ofn)))
+                print(f"[parity] rkc_step {name} box {sid} h={h} s={s}: d rel {ed:.3g}, f rel {ef:.3g}")
+                assert ed <= 1e-12 and ef <= 1e-12, (name, sid, h, s, ed, ef)
