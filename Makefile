@@ -33,7 +33,7 @@ build/plan.o: $(SRC)/plan.cu $(SRC)/ddpma_internal.h include/ddpma.h | build
 build/kernels.o: $(SRC)/kernels.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(SRC)/fastlog.cuh $(SRC)/logtable.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/kernels.ptxas.log || (cat build/kernels.ptxas.log; false)
 
-build/persist.o: $(SRC)/persist.cu $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(SRC)/fastlog.cuh $(SRC)/logtable.h | build
+build/persist.o: $(SRC)/persist.cu $(SRC)/crpow.cuh $(SRC)/ddpma_internal.h $(SRC)/stencil.cuh $(SRC)/fastlog.cuh $(SRC)/logtable.h | build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/persist.ptxas.log || (cat build/persist.ptxas.log; false)
 
 $(OUT): $(OBJ)

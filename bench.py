@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ddpma", choices=["ddpma", "reference"])
     ap.add_argument("--profile", default="default", choices=["default", "stable"])
+    ap.add_argument("--until-tol", type=float, default=None,
+                    help="time-to-converged mode: run windows until the stop rule meets TOL")
+    ap.add_argument("--max-windows", type=int, default=5000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -133,6 +136,13 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def kernel_name(dim):
+    if dim == 2 and os.environ.get("DDPMA_KERNEL", "D")[:1] != "P":
+        return ("k_windowD<pow2> persistent dataflow window kernel (RKC2 steps as level x item "
+                "task sweeps, TMA tile ring; 48 B/node-update at stage j>=4)")
+    return f"k_windowP<{dim},pow2> persistent window kernel (stage-by-stage actions)"
+
+
 def peaks():
     try:
         with open(PEAKS) as f:
@@ -143,9 +153,17 @@ def peaks():
 
 
 def ncu_traffic():
+    """DRAM bytes per node-update of the window kernel from the committed ncu
+    --set full summary -- only if it was captured on the current kernel
+    source (sha256 of csrc/persist.cu), else None."""
+    import hashlib
     try:
         with open(NCU_SUMMARY) as f:
             d = json.load(f)
+        src = os.path.join(REPO, "paper_2006_14602_b200", "csrc", "persist.cu")
+        sha = hashlib.sha256(open(src, "rb").read()).hexdigest()
+        if d.get("persist_cu_sha256") != sha:
+            return None, d
         return d.get("stage_traffic_bytes_per_node"), d
     except Exception:
         return None, None
@@ -310,10 +328,7 @@ def run_gpu(args):
                if traffic_per_node else None)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": ("k_windowW<pow2> persistent warp-specialised window kernel: fused "
-                           "RHS + RKC2 stage / final / f0 / power actions (48 B/node-update at "
-                           "stage j>=4)" if os.environ.get("DDPMA_WS", "0") != "0" else
-                           "k_windowP<2,pow2> persistent window kernel"),
+                "kernel": kernel_name(g.dim),
                 "algo_bytes_per_launch": prof["bytes"][k] / max(1, int(prof["launches"][k])),
                 "avg_launch_ms": prof["ms"][k] / max(1, int(prof["launches"][k])),
                 "share_of_step": round(share, 4), "peak_source": peak_src}
@@ -380,10 +395,66 @@ def run_gpu(args):
         torch.distributed.destroy_process_group()
 
 
+def run_until_tol(args):
+    """Time-to-converged mesh (BASELINE metric, second half): the public
+    solve() runs windows until min/max subdomain residual <= tol
+    (schwarz.py:318,333,340).  Device time = CUDA events around the window
+    loop on the plan stream; e2e = wall time of P.solve() with a host psi0
+    (plan build, H2D, windows, assembly, D2H)."""
+    import torch
+    import paper_2006_14602_b200 as P
+    from paper_2006_14602_b200.plan import Plan
+    torch.cuda.set_device(0)
+    g, dec, mon = case(args.config, P)
+    kw = dict(tol=args.until_tol, max_windows=args.max_windows, transmission="parallel")
+    if args.profile == "stable":
+        kw.update(rtol=1e-6, atol=1e-9)
+    cfg = P.SolverConfig(**kw)
+    plan = Plan.for_grid(g, dec.subdomains, mon, cfg)
+    plan.set_state(None)
+    stream = torch.cuda.ExternalStream(P._lib.lib().ddpma_stream(plan.h))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        w, conv, fres, hres, hstats = plan.run(args.max_windows, args.until_tol)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    dev_s = e0.elapsed_time(e1) / 1e3
+    c = plan.counters()
+    jmin = float(np.min(hstats[:, 1])) if len(hstats) else None
+    plan.close()
+    t0 = time.perf_counter()
+    res = P.solve(g, dec, mon, cfg)
+    wall = time.perf_counter() - t0
+    line = {"metric": "time-to-converged mesh", "value": dev_s, "unit": "s",
+            "higher_is_better": False, "n_gpus": 1, "dtype": "f64",
+            "data": "synthetic (seeded Gaussian-mixture / ring monitor, psi0 = |xi|^2/2)",
+            "config": {"workload": args.config, "profile": args.profile, "tol": args.until_tol,
+                       "stop_rule": "min", "transmission": "parallel",
+                       "max_windows": args.max_windows},
+            "converged": bool(conv), "windows": int(w), "final_residual": float(fres),
+            "time_to_converged_s": dev_s if conv else None,
+            "node_updates": int(c["node_updates"]),
+            "node_updates_per_s": c["node_updates"] / dev_s if dev_s > 0 else None,
+            "min_jac_over_windows": jmin,
+            "e2e": {"value": wall, "unit": "s", "converged": bool(res.converged),
+                    "windows": int(res.windows),
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step":
+                        (res.psi.nbytes + res.mesh.coords.nbytes + res.mesh.jac.nbytes
+                         + sum(x.nbytes for x in res.sub_psi)) / max(1, res.windows),
+                    "note": "public solve(): plan build, psi0, windows to tol, assembly, D2H"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.until_tol is not None:
+        run_until_tol(args)
     else:
         run_gpu(args)
 

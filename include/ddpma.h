@@ -331,6 +331,13 @@ ddpma_status ddpma_relative_errors(ddpma_plan* plan, int sub_id, const double* p
 ddpma_status ddpma_counters(const ddpma_plan* plan, int64_t* node_updates,
                             int64_t* rhs_evals, int64_t* launches,
                             double* algo_bytes);
+/* Owned blocks of the LOCAL subdomains (ascending id) packed into one device
+ * buffer for the multi-GPU gather (replaces the reference's in-process
+ * _assemble copies, schwarz.py:271-282): subdomain by subdomain, its owned
+ * range in C order as [psi | coords (interleaved dim) | jac].  *size
+ * receives the element count; out_dev may be NULL to query it. */
+ddpma_status ddpma_pack_owned(ddpma_plan* plan, double* out_dev, int64_t* size);
+
 /* RHS evaluations per LOCAL subdomain (ascending global id) since the last
  * ddpma_set_state: the device controller's tally of Rkc2Integrator /
  * EulerIntegrator right-hand-side calls (integrate.py:163-250), i.e. the

@@ -102,6 +102,7 @@ SIGNATURES = {
                                  _D, _D, _I, _I]),
     "ddpma_counters": (C.c_int, [_P, _I64, _I64, _I64, _D]),
     "ddpma_integrate_window": (C.c_int, [_P, C.c_int, _D, _D, C.c_double]),
+    "ddpma_pack_owned": (C.c_int, [_P, C.c_void_p, _I64]),
     "ddpma_sub_evals": (C.c_int, [_P, _I64, C.c_int]),
     "ddpma_set_profiling": (C.c_int, [_P, C.c_int]),
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),

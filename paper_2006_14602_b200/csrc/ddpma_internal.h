@@ -86,6 +86,11 @@ struct SubGeo {
   int olo[3], ohi[3];    // owned range, box-local inclusive
   long long nodes;
   int items_x, items_y, items_z, nitems;   // persistent-kernel work items
+  // dataflow sweeps (persist.cu k_windowD): items are grouped in rows of
+  // `ipr` consecutive items (2D: one item row; 3D: one item plane); rowprog
+  // [rowoff + r] counts the completed sweep tasks of row r
+  long long rowoff;
+  int ipr, nrows;
 };
 
 constexpr int IR2 = 16;   // 2D work item: TX x IR2 nodes (each thread IR2/TY rows)
@@ -137,7 +142,9 @@ enum Mode {
   M_POWER = 5,     // power-iteration eval (:139-141)
   M_POWER_SEED = 6,// first power-iteration eval from the checkerboard seed
   M_EULER = 7,     // y + (dtau/m)*F(y)                  (:69-74)
-  M_NORM = 8       // sum y^2 (np.linalg.norm(y), :133)
+  M_NORM = 8,      // sum y^2 (np.linalg.norm(y), :133)
+  M_SWEEP = 9      // one whole RKC2 step: stages 2..s + final as a dataflow
+                   // of (level, item) tasks (persist.cu k_windowD)
 };
 
 struct KArgs {
@@ -171,14 +178,17 @@ struct DevCtl {
   int fail_status, fail_nonfin, fail_s, fail_yi;
   int fail_fi, pad1, pad2, pad3;
   double fail_t, fail_h, fail_h04;
-  // current action (valid for sequence number word >> 32)
+  // current action (valid for sequence number word >> 48)
   int a_mode, a_j, a_s, a_yi;
-  int a_fi, a_vin, a_vout, a_pad;
+  int a_fi, a_vin, a_vout, a_ntasks;
   double a_c, a_h04, a_mu, a_nu, a_hmut, a_hgt;
+  double a_h;                    // SWEEP: step size (per-level h*mut_j, h*gt_j)
+  unsigned long long a_sbase;    // SWEEP: rowprog value of every row at its start
+  unsigned long long sbase;      // rowprog base of the next sweep
   // per-action accumulators and synchronisation words
   unsigned int acc_flags, done;
   unsigned long long acc_emax;
-  unsigned long long word;       // (seq << 32) | claim cursor
+  unsigned long long word;       // (seq << 48) | (ntasks << 24) | claim cursor
   long long evals;               // RHS evaluations (node-updates / box nodes)
   double bytes;                  // algorithmic bytes moved
   unsigned long long t_begin, t_done;   // %globaltimer at window begin / subdomain done
@@ -212,13 +222,27 @@ struct WinArgs {
   int chunk_bulk;            // items per claim while >= tail_n subdomains are active
   int chunk_tail, tail_n;    // items per claim below that (the tail's critical path)
   const void* tmap;          // 2D: CUtensorMap[nlocal][8 fields][2 boxes] (TMA tile loads), or null
+  int sweep;                 // 1: RKC2 steps run as M_SWEEP dataflow actions (k_windowD)
+  int proxy_fence;           // fence.proxy.async.global before TMA reads of generic writes
+  unsigned long long* rowprog;   // per-row completed sweep tasks (SubGeo::rowoff)
 };
+
+// Synchronisation word of a subdomain's current action: 16-bit sequence
+// number, 24-bit task count, 24-bit claim cursor.  A finished subdomain
+// publishes ntasks = 0, so it is never claimable, and stray claim
+// increments (claimers that scanned before the publish) stay in the cursor
+// field: 2^24 - ntasks of slack.
+constexpr int kWordCurBits = 24;
+constexpr unsigned long long kWordCurMask = (1ull << kWordCurBits) - 1ull;
+constexpr unsigned kMaxTasks = 1u << 22;   // ntasks limit (leaves >= 12M of cursor slack)
 
 // fields addressable by the window kernel's tensor maps
 enum { TF_Y0 = 0, TF_Y1, TF_F0, TF_F1, TF_D0, TF_D1, TF_D2, TF_MR, TF_N };
 
 void launch_window(const WinArgs& a, int nblocks, void* stream);
+void launch_pack_owned(const KArgs& a, int nb, double* out, const long long* offs, void* stream);
 int window_blocks(int dim, int pow2);   // co-resident CTAs for the cooperative launch
+bool window_dataflow(int dim);           // k_windowD (M_SWEEP actions) runs this dimension
 void launch_window_begin(const WinArgs& a, void* stream);
 
 struct FaceJob {

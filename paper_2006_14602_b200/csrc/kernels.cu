@@ -400,6 +400,36 @@ __global__ void __launch_bounds__(NT) k_assemble(const KArgs a, double* psi, dou
   if (jac) jac[gk] = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
 }
 
+// Owned blocks of the local subdomains, packed for the multi-GPU gather
+// (SURVEY §8(e)): subdomain l occupies out[offs[l] ..) as [psi | coords
+// (interleaved) | jac] over its owned range in C order, the same values
+// k_assemble writes into the global arrays (schwarz.py:271-282).
+template <int DIM, bool P2>
+__global__ void __launch_bounds__(NT) k_pack_owned(const KArgs a, double* out,
+                                                   const long long* offs) {
+  const int b = blockIdx.x;
+  const Entry e = a.ent[find_entry(a.ent, a.nent, b)];
+  const SubGeo& g = a.geo[e.sub];
+  int i0, i1, i2;
+  if (!tile_node<DIM>(g, b - e.tile_begin, i0, i1, i2)) return;
+  const int idx[3] = {i0, i1, i2};
+  long long o = 0, on = 1;
+#pragma unroll
+  for (int q = 0; q < DIM; ++q) {
+    if (idx[q] < g.olo[q] || idx[q] > g.ohi[q]) return;
+    const long long n = g.ohi[q] - g.olo[q] + 1;
+    o = o * n + (idx[q] - g.olo[q]);
+    on *= n;
+  }
+  double* base = out + offs[e.sub];
+  const double* yb = a.F.y[e.yi];
+  const YAcc<DIM, YM_PLAIN> Y{&g, yb, nullptr, 0.0};
+  base[o] = yb[lin<DIM>(g, i0, i1, i2)];
+#pragma unroll
+  for (int q = 0; q < DIM; ++q) base[on + o * DIM + q] = coord<DIM, P2>(a.P, g, q, i0, i1, i2, Y);
+  base[on * (1 + DIM) + o] = hdet<DIM, P2>(a.P, g, i0, i1, i2, Y);
+}
+
 // Dense box outputs of gradient_fd / hessian_det_fd / mesh_density for the
 // operator-level API (pma.py:67-84,133-149; monitor.py:151-180).
 template <int DIM, bool P2>
@@ -646,6 +676,19 @@ void launch_assemble(const KArgs& a, int nb, double* psi, double* coords, double
   } else {
     if (a.P.pow2) k_assemble<3, true><<<nb, blk, 0, st>>>(a, psi, coords, jac);
     else k_assemble<3, false><<<nb, blk, 0, st>>>(a, psi, coords, jac);
+  }
+}
+
+void launch_pack_owned(const KArgs& a, int nb, double* out, const long long* offs, void* stream) {
+  if (nb <= 0) return;
+  const dim3 blk(TX, TY);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a.P.dim == 2) {
+    if (a.P.pow2) k_pack_owned<2, true><<<nb, blk, 0, st>>>(a, out, offs);
+    else k_pack_owned<2, false><<<nb, blk, 0, st>>>(a, out, offs);
+  } else {
+    if (a.P.pow2) k_pack_owned<3, true><<<nb, blk, 0, st>>>(a, out, offs);
+    else k_pack_owned<3, false><<<nb, blk, 0, st>>>(a, out, offs);
   }
 }
 

@@ -27,6 +27,7 @@
 
 #include "ddpma_internal.h"
 #include "stencil.cuh"
+#include "crpow.cuh"
 
 #ifndef DDPMA_MINB2
 #define DDPMA_MINB2 4   // resident CTAs per SM of the 2D window kernel (register cap)
@@ -45,10 +46,16 @@ enum { R_START = 0, R_ACCEPT, R_REJECT };
 constexpr double kSqrtEps = 1.4901161193847656e-08;   // np.sqrt(np.finfo(float).eps)
 constexpr double kStab = 0.653;                       // integrate.py:36
 constexpr double kMinStep = 1e-14;                    // integrate.py:37
-// Low half of a finished subdomain's synchronisation word.  Far from 2^32 so
-// that stray claim increments (a claimer that scanned the word before the
-// publish) can never carry into the sequence half and make it claimable.
-constexpr unsigned long long kDoneLow = 0x80000000ull;
+__device__ __forceinline__ unsigned w_cursor(unsigned long long w) {
+  return (unsigned)(w & kWordCurMask);
+}
+__device__ __forceinline__ unsigned w_ntasks(unsigned long long w) {
+  return (unsigned)((w >> kWordCurBits) & kWordCurMask);
+}
+__device__ __forceinline__ unsigned long long w_seq(unsigned long long w) { return w >> 48; }
+__device__ __forceinline__ unsigned long long w_make(unsigned long long seq, unsigned ntasks) {
+  return (seq << 48) | ((unsigned long long)ntasks << kWordCurBits);
+}
 
 // Shared-memory copy of the log table (filled at the start of k_windowP;
 // the table lookups are the fp64 log's only memory accesses).
@@ -81,22 +88,6 @@ struct GAcc {   // Y from global memory (boundary nodes), coherent loads
   }
 };
 
-struct SAcc2 {   // 2D smem tile with a 1-node halo
-  const double* s;
-  int r0, c0;
-  __device__ __forceinline__ double operator()(int i0, int i1, int) const {
-    return s[(i0 - r0 + 1) * (TX + 2) + (i1 - c0 + 1)];
-  }
-};
-
-struct SAcc3 {   // 3D smem tile with a 1-node halo
-  const double* s;
-  int z0, r0, c0;
-  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
-    return s[((i0 - z0 + 1) * (TY + 2) + (i1 - r0 + 1)) * (TX + 2) + (i2 - c0 + 1)];
-  }
-};
-
 struct Act {      // the action of the claimed item (broadcast through smem)
   int mode, j, s, yi, fi, vin, vout, sub;
   double c, h04, mu, nu, hmut, hgt;
@@ -121,256 +112,6 @@ __device__ __forceinline__ double ymake(double yv, double av, double c, int par)
 }
 
 // One node: RHS (pma_rhs_frozen) + the consuming epilogue of the action.
-template <int DIM, bool P2, int MODE, int YM, class SA>
-__device__ __forceinline__ void node(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
-                                     int i1, int i2, const SA& S, const double* aptr, Acc& acc) {
-  const long long k = lin<DIM>(g, i0, i1, i2);
-  const double* yb = A.F.y[t.yi];
-  if constexpr (MODE == M_NORM) {
-    const double y = ldc(yb + k);
-    acc.psum += y * y;
-    return;
-  } else {
-    const bool dir = dirichlet<DIM>(g, i0, i1, i2);
-    bool interior = i0 >= 1 && i0 <= g.n[0] - 2 && i1 >= 1 && i1 <= g.n[1] - 2;
-    if constexpr (DIM == 3) interior = interior && i2 >= 1 && i2 <= g.n[2] - 2;
-    double det;
-    if (interior) det = hdet<DIM, P2>(A.P, g, i0, i1, i2, S);
-    else det = hdet<DIM, P2>(A.P, g, i0, i1, i2, GAcc<DIM, YM>{&g, yb, aptr, t.c});
-    const double F = dir ? 0.0 : logequi(ldc(A.F.mr + k), det, A.P.guard, A.P.floor, A.P.rguard);
-    acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
-    if constexpr (MODE == M_F0) {
-      A.F.f[t.fi][k] = F;
-    } else if constexpr (MODE == M_EULER) {
-      A.F.y[1 - t.yi][k] = ldc(yb + k) + t.c * F;
-    } else if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
-      const double f0 = ldc(A.F.f[t.fi] + k);
-      const double d1 = t.c * f0;
-      double dp, dp2;
-      if constexpr (MODE == M_STAGE2) {
-        dp = d1;
-        dp2 = 0.0;
-      } else if constexpr (MODE == M_STAGE3) {
-        dp = ldc(A.F.d[2] + k);
-        dp2 = d1;
-      } else {
-        dp = ldc(A.F.d[(t.j - 1) % 3] + k);
-        dp2 = ldc(A.F.d[(t.j - 2) % 3] + k);
-      }
-      A.F.d[t.j % 3][k] = ((t.mu * dp + t.nu * dp2) + t.hmut * F) + t.hgt * f0;
-    } else if constexpr (MODE == M_FINAL) {
-      const double ds = ldc(A.F.d[t.s % 3] + k);
-      const double yv = ldc(yb + k);
-      const double yn = yv + ds;
-      const double f0 = ldc(A.F.f[t.fi] + k);
-      A.F.f[1 - t.fi][k] = F;
-      A.F.y[1 - t.yi][k] = yn;
-      const double err = -0.8 * ds + t.h04 * (f0 + F);
-      const double ay = fabs(yv), an = fabs(yn);
-      const double mx = (ay >= an || isnan(ay)) ? ay : an;
-      const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
-      if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
-      else acc.nonfin = 1;
-    } else {
-      const double diff = F - ldc(A.F.f[t.fi] + k);
-      A.F.d[t.vout][k] = diff;
-      acc.psum += diff * diff;
-    }
-  }
-}
-
-// Interior 2D Hessian determinant straight from the smem tile: the interior
-// formulas of hessian_det_fd (pma.py:87-140, np.gradient interior) in the
-// same evaluation order as hdet's interior branch (bitwise identical).
-template <bool P2>
-__device__ __forceinline__ double hdet2_fast(const Prob& P, const double* p) {
-  constexpr int W = TX + 2;
-  const double c = p[0];
-  const double h00 = dv<P2>((p[W] - 2.0 * c) + p[-W], P.ax[0].hh, P.ax[0].ihh);
-  const double h11 = dv<P2>((p[1] - 2.0 * c) + p[-1], P.ax[1].hh, P.ax[1].ihh);
-  const double gp = dv<P2>(p[W + 1] - p[W - 1], P.ax[1].twoh, P.ax[1].itwoh);
-  const double gm = dv<P2>(p[-W + 1] - p[-W - 1], P.ax[1].twoh, P.ax[1].itwoh);
-  const double h01 = dv<P2>(gp - gm, P.ax[0].twoh, P.ax[0].itwoh);
-  return h00 * h11 - h01 * h01;
-}
-
-// One 2D work item: TX x IR2 nodes, each thread IR2/TY rows.  Center values
-// are prefetched first, then the tile + halo of Y is staged in smem, then the
-// nodes are evaluated (interior: smem stencil; box faces: generic path).
-template <bool P2, int MODE, int YM>
-__device__ void item2(const WinArgs& A, const SubGeo& g, const Act& t, int item, double* sY,
-                      Acc& acc) {
-  constexpr int W = TX + 2, H = IR2 + 2, R = IR2 / TY;
-  const int ix = item % g.items_x, iy = item / g.items_x;
-  const int c0 = ix * TX, r0 = iy * IR2;
-  const int n0 = g.n[0], n1 = g.n[1];
-  const double* yb = A.F.y[t.yi];
-  const double* ap = nullptr;
-  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
-  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
-  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
-  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
-  constexpr bool NEED_F0 = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN ||
-                           MODE == M_FINAL || MODE == M_POWER || MODE == M_POWER_SEED;
-  constexpr bool NEED_Y = MODE == M_FINAL || MODE == M_EULER || MODE == M_NORM;
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  const int i1 = c0 + threadIdx.x;
-  double cm[R], cf[R], cd[R], cd2[R], cy[R];
-  bool ok[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int i0 = r0 + threadIdx.y + q * TY;
-    ok[q] = i1 < n1 && i0 < n0;
-    cm[q] = cf[q] = cd[q] = cd2[q] = cy[q] = 0.0;
-    if (ok[q]) {
-      const long long k = g.off + (long long)i0 * g.pitch + i1;
-      if constexpr (MODE != M_NORM) cm[q] = ldc(A.F.mr + k);
-      if constexpr (NEED_F0) cf[q] = ldc(A.F.f[t.fi] + k);
-      if constexpr (MODE == M_STAGE3) cd[q] = ldc(A.F.d[2] + k);
-      if constexpr (MODE == M_STAGEN) {
-        cd[q] = ldc(A.F.d[(t.j - 1) % 3] + k);
-        cd2[q] = ldc(A.F.d[(t.j - 2) % 3] + k);
-      }
-      if constexpr (MODE == M_FINAL) cd[q] = ldc(A.F.d[t.s % 3] + k);
-      if constexpr (NEED_Y) cy[q] = ldc(yb + k);
-    }
-  }
-  if constexpr (MODE != M_NORM) {
-#pragma unroll
-    for (int it = 0; it < (W * H + NT - 1) / NT; ++it) {
-      const int e = tid + it * NT;
-      if (e < W * H) {
-        const int rr = e / W, cc = e - rr * W;
-        const int i0 = r0 - 1 + rr, j1 = c0 - 1 + cc;
-        double v = 0.0;
-        if (i0 >= 0 && i0 < n0 && j1 >= 0 && j1 < n1) {
-          const long long k = g.off + (long long)i0 * g.pitch + j1;
-          const double av = (YM == YM_ADD || YM == YM_SCALED) ? ldc(ap + k) : 0.0;
-          v = ymake<YM>(ldc(yb + k), av, t.c, (i0 + j1) & 1);
-        }
-        sY[e] = v;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    if (!ok[q]) continue;
-    const int i0 = r0 + threadIdx.y + q * TY;
-    const long long k = g.off + (long long)i0 * g.pitch + i1;
-    if constexpr (MODE == M_NORM) {
-      acc.psum += cy[q] * cy[q];
-    } else {
-      const bool dir = dirichlet<2>(g, i0, i1, 0);
-      const bool interior = i0 >= 1 && i0 <= n0 - 2 && i1 >= 1 && i1 <= n1 - 2;
-      double det;
-      if (interior) det = hdet2_fast<P2>(A.P, sY + (threadIdx.y + q * TY + 1) * W + threadIdx.x + 1);
-      else det = hdet<2, P2>(A.P, g, i0, i1, 0, GAcc<2, YM>{&g, yb, ap, t.c});
-      const double F = dir ? 0.0 : logequi(cm[q], det, A.P.guard, A.P.floor, A.P.rguard);
-      acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
-      if constexpr (MODE == M_F0) {
-        A.F.f[t.fi][k] = F;
-      } else if constexpr (MODE == M_EULER) {
-        A.F.y[1 - t.yi][k] = cy[q] + t.c * F;
-      } else if constexpr (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN) {
-        const double f0 = cf[q];
-        const double d1 = t.c * f0;
-        double dp, dp2;
-        if constexpr (MODE == M_STAGE2) {
-          dp = d1;
-          dp2 = 0.0;
-        } else if constexpr (MODE == M_STAGE3) {
-          dp = cd[q];
-          dp2 = d1;
-        } else {
-          dp = cd[q];
-          dp2 = cd2[q];
-        }
-        A.F.d[t.j % 3][k] = ((t.mu * dp + t.nu * dp2) + t.hmut * F) + t.hgt * f0;
-      } else if constexpr (MODE == M_FINAL) {
-        const double ds = cd[q], yv = cy[q], f0 = cf[q];
-        const double yn = yv + ds;
-        A.F.f[1 - t.fi][k] = F;
-        A.F.y[1 - t.yi][k] = yn;
-        const double err = -0.8 * ds + t.h04 * (f0 + F);
-        const double ay = fabs(yv), an = fabs(yn);
-        const double mx = (ay >= an || isnan(ay)) ? ay : an;
-        const double r = fabs(err) / (A.P.atol + A.P.rtol * mx);
-        if (isfinite(r)) acc.ratio = r > acc.ratio ? r : acc.ratio;
-        else acc.nonfin = 1;
-      } else {
-        const double diff = F - cf[q];
-        A.F.d[t.vout][k] = diff;
-        acc.psum += diff * diff;
-      }
-    }
-  }
-}
-
-// One 3D work item: TX x TY x IZ3 nodes; tile + halo staged in smem.
-template <bool P2, int MODE, int YM>
-__device__ void item3(const WinArgs& A, const SubGeo& g, const Act& t, int item, double* sY,
-                      Acc& acc) {
-  const int ix = item % g.items_x;
-  const int r = item / g.items_x;
-  const int iy = r % g.items_y, iz = r / g.items_y;
-  const int c0 = ix * TX, r0 = iy * TY, z0 = iz * IZ3;
-  const double* yb = A.F.y[t.yi];
-  const double* ap = nullptr;
-  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
-  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
-  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
-  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  if constexpr (MODE != M_NORM) {
-    constexpr int W = TX + 2, H = TY + 2, D = IZ3 + 2;
-    for (int e = tid; e < W * H * D; e += NT) {
-      const int cc = e % W, rr = (e / W) % H, zz = e / (W * H);
-      const int i0 = z0 - 1 + zz, i1 = r0 - 1 + rr, i2 = c0 - 1 + cc;
-      double v = 0.0;
-      if (i0 >= 0 && i0 < g.n[0] && i1 >= 0 && i1 < g.n[1] && i2 >= 0 && i2 < g.n[2]) {
-        const long long k = g.off + ((long long)i0 * g.n[1] + i1) * g.pitch + i2;
-        const double av = (YM == YM_ADD || YM == YM_SCALED) ? ldc(ap + k) : 0.0;
-        v = ymake<YM>(ldc(yb + k), av, t.c, (i0 + i1 + i2) & 1);
-      }
-      sY[e] = v;
-    }
-    __syncthreads();
-  }
-  const SAcc3 S{sY, z0, r0, c0};
-  const int i2 = c0 + threadIdx.x, i1 = r0 + threadIdx.y;
-  if (i1 < g.n[1] && i2 < g.n[2]) {
-    for (int q = 0; q < IZ3; ++q) {
-      const int i0 = z0 + q;
-      if (i0 < g.n[0]) node<3, P2, MODE, YM>(A, g, t, i0, i1, i2, S, ap, acc);
-    }
-  }
-}
-
-template <int DIM, bool P2, int MODE, int YM>
-__device__ __forceinline__ void run_item(const WinArgs& A, const SubGeo& g, const Act& t, int item,
-                                         double* sY, Acc& acc) {
-  if constexpr (DIM == 2) item2<P2, MODE, YM>(A, g, t, item, sY, acc);
-  else item3<P2, MODE, YM>(A, g, t, item, sY, acc);
-}
-
-template <int DIM, bool P2>
-__device__ void dispatch_item(const WinArgs& A, const SubGeo& g, const Act& t, int item,
-                              double* sY, Acc& acc) {
-  switch (t.mode) {
-    case M_F0: run_item<DIM, P2, M_F0, YM_PLAIN>(A, g, t, item, sY, acc); break;
-    case M_EULER: run_item<DIM, P2, M_EULER, YM_PLAIN>(A, g, t, item, sY, acc); break;
-    case M_STAGE2: run_item<DIM, P2, M_STAGE2, YM_SCALED>(A, g, t, item, sY, acc); break;
-    case M_STAGE3: run_item<DIM, P2, M_STAGE3, YM_ADD>(A, g, t, item, sY, acc); break;
-    case M_STAGEN: run_item<DIM, P2, M_STAGEN, YM_ADD>(A, g, t, item, sY, acc); break;
-    case M_FINAL: run_item<DIM, P2, M_FINAL, YM_ADD>(A, g, t, item, sY, acc); break;
-    case M_POWER: run_item<DIM, P2, M_POWER, YM_SCALED>(A, g, t, item, sY, acc); break;
-    case M_POWER_SEED: run_item<DIM, P2, M_POWER_SEED, YM_SEED>(A, g, t, item, sY, acc); break;
-    case M_NORM: run_item<DIM, P2, M_NORM, YM_PLAIN>(A, g, t, item, sY, acc); break;
-    default: break;
-  }
-}
-
 __device__ __forceinline__ double mode_bytes_d(int mode) {
   switch (mode) {
     case M_F0: return 24.0;
@@ -484,9 +225,19 @@ __device__ void d_start_sigma(DevCtl& c, int ret) {
 __device__ void d_complete(const WinArgs& A, DevCtl& c, int l, double sum, long long nodes) {
   const double total = A.dtau;
   const int gid = A.geo[l].gid;
-  const int mode = c.a_mode;
-  c.bytes += mode_bytes_d(mode) * (double)nodes;
-  if (mode != M_NORM) c.evals += 1;
+  int mode = c.a_mode;
+  if (mode == M_SWEEP) {   // stages 2..s and the final evaluation of one step
+    const int s = c.a_s;
+    c.bytes += (32.0 + (s >= 3 ? 40.0 : 0.0) + 48.0 * (double)(s - 3 > 0 ? s - 3 : 0) + 48.0) *
+               (double)nodes;
+    c.evals += s;
+    c.sbase += (unsigned long long)s * (unsigned long long)A.geo[l].ipr;
+    c.step_flag = (c.acc_flags & 1u) ? 1 : 0;
+    mode = M_FINAL;
+  } else {
+    c.bytes += mode_bytes_d(mode) * (double)nodes;
+    if (mode != M_NORM) c.evals += 1;
+  }
   switch (mode) {
     case M_STAGE2:
     case M_STAGE3:
@@ -550,7 +301,7 @@ __device__ void d_complete(const WinArgs& A, DevCtl& c, int l, double sum, long 
         const bool need = c.since >= c.interval && c.t < total;
         double grow = 5.0;
         if (emax != 0.0) {
-          const double gg = 0.8 * pow(emax, -1.0 / 3.0);
+          const double gg = 0.8 * pow_m13_rn(emax);   // crpow.cuh: glibc-faithful pow
           grow = gg < 5.0 ? gg : 5.0;
         }
         c.h = c.h * (0.1 < grow ? grow : 0.1);
@@ -566,7 +317,7 @@ __device__ void d_complete(const WinArgs& A, DevCtl& c, int l, double sum, long 
           c.h *= 0.5;
           c.rej_row += 1;
         } else {
-          const double gg = 0.8 * pow(emax, -1.0 / 3.0);
+          const double gg = 0.8 * pow_m13_rn(emax);   // crpow.cuh: glibc-faithful pow
           c.h *= (0.1 < gg ? gg : 0.1);
           c.rej_row += 1;
         }
@@ -593,10 +344,11 @@ __device__ void d_complete(const WinArgs& A, DevCtl& c, int l, double sum, long 
 
 // Fill the action fields from the phase (the next action of the subdomain).
 // Returns false when the subdomain has finished (DONE / FAILED).
-__device__ bool d_next_action(const WinArgs& A, DevCtl& c) {
+__device__ bool d_next_action(const WinArgs& A, DevCtl& c, int nitems) {
   c.a_yi = c.yi;
   c.a_fi = c.fi;
   c.a_s = c.s;
+  c.a_ntasks = nitems;
   switch (c.phase) {
     case P_F0:
       c.a_mode = M_F0;
@@ -618,6 +370,14 @@ __device__ bool d_next_action(const WinArgs& A, DevCtl& c) {
       }
       const int base = A.coef_off[c.s];
       c.a_c = c.h * A.coef[4 * base + 0];      // h * mu1_t
+      if (A.sweep) {   // the whole step (stages 2..s, final) as one dataflow action
+        c.a_mode = M_SWEEP;
+        c.a_h = c.h;
+        c.a_h04 = 0.4 * c.h;
+        c.a_sbase = c.sbase;
+        c.a_ntasks = c.s * nitems;
+        return true;
+      }
       if (c.j <= c.s) {
         const int j = c.j;
         c.a_mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
@@ -659,185 +419,22 @@ __device__ __forceinline__ void ctl_store(DevCtl* dst, const DevCtl& src) {
 }
 
 // Publish the next action of subdomain l from the private copy c (thread 0).
-__device__ void d_publish(const WinArgs& A, DevCtl& c, DevCtl* gc) {
-  const unsigned long long seq = (c.word >> 32) + 1;
-  const bool more = d_next_action(A, c);
+__device__ void d_publish(const WinArgs& A, DevCtl& c, DevCtl* gc, int nitems) {
+  const unsigned long long seq = w_seq(c.word) + 1;
+  const bool more = d_next_action(A, c, nitems);
   c.acc_flags = 0;
   c.acc_emax = 0ull;
   c.done = 0;
   ctl_store(gc, c);
   __threadfence();
   if (more) {
-    atomicExch(&gc->word, seq << 32);
+    atomicExch(&gc->word, w_make(seq, (unsigned)c.a_ntasks));
   } else {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     __stcg(reinterpret_cast<long long*>(&gc->t_done), (long long)now);
-    atomicExch(&gc->word, (seq << 32) | kDoneLow);
+    atomicExch(&gc->word, w_make(seq, 0u));
     atomicAdd(A.n_done, 1u);
-  }
-}
-
-__device__ __forceinline__ double block_sum2(double v, double* sh) {
-  return block_sum(v, sh);
-}
-
-template <int DIM, bool P2>
-__global__ void __launch_bounds__(NT, DIM == 2 ? 4 : 2) k_window(const WinArgs A) {
-  constexpr int SM_ELEMS = DIM == 2 ? (TX + 2) * (IR2 + 2) : (TX + 2) * (TY + 2) * (IZ3 + 2);
-  __shared__ double sY[SM_ELEMS];
-  __shared__ double sh_sum[NT / 32];
-  __shared__ unsigned long long sh_max[NT / 32];
-  __shared__ Act s_act;
-  __shared__ DevCtl s_ctl;
-  __shared__ int s_sub, s_item, s_exit, s_last;
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  unsigned backoff = 32;
-  while (true) {
-    // Warp 0 claims the next item: subdomains are scanned in PRIORITY order
-    // (A.act is sorted by the previous window's work, the straggler first),
-    // 32 candidates per round in parallel; the first claimable one wins.
-    if (threadIdx.y == 0) {
-      const int lane = threadIdx.x;
-      int got = -1, item = 0;
-      for (int base = 0; base < A.nact && got < 0; base += 32) {
-        const int q = base + lane;
-        int l = -1;
-        bool claimable = false;
-        if (q < A.nact) {
-          l = A.act[q];
-          const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
-          claimable = (unsigned)(w & 0xffffffffull) < (unsigned)A.geo[l].nitems;
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, claimable);
-        while (mask != 0u && got < 0) {
-          const int src = __ffs(mask) - 1;
-          mask &= mask - 1u;
-          int it = -1;
-          if (lane == src) {
-            const unsigned long long w2 = atomicAdd(&A.ctl[l].word, 1ull);
-            const unsigned u = (unsigned)(w2 & 0xffffffffull);
-            if (u < (unsigned)A.geo[l].nitems) it = (int)u;
-          }
-          it = __shfl_sync(0xffffffffu, it, src);
-          if (it >= 0) {
-            got = __shfl_sync(0xffffffffu, l, src);
-            item = it;
-          }
-        }
-      }
-      if (lane == 0) {
-        s_sub = got;
-        s_item = item;
-        s_exit = 0;
-        if (got < 0) {
-          s_exit = *(volatile unsigned*)A.n_done >= (unsigned)A.nact;
-        } else {
-          __threadfence();   // acquire: the action and the previous action's data
-          const DevCtl* gc = A.ctl + got;
-          Act t;
-          t.mode = __ldcg(&gc->a_mode);
-          t.j = __ldcg(&gc->a_j);
-          t.s = __ldcg(&gc->a_s);
-          t.yi = __ldcg(&gc->a_yi);
-          t.fi = __ldcg(&gc->a_fi);
-          t.vin = __ldcg(&gc->a_vin);
-          t.vout = __ldcg(&gc->a_vout);
-          t.sub = got;
-          t.c = __ldcg(&gc->a_c);
-          t.h04 = __ldcg(&gc->a_h04);
-          t.mu = __ldcg(&gc->a_mu);
-          t.nu = __ldcg(&gc->a_nu);
-          t.hmut = __ldcg(&gc->a_hmut);
-          t.hgt = __ldcg(&gc->a_hgt);
-          s_act = t;
-        }
-      }
-    }
-    __syncthreads();
-    if (s_sub < 0) {
-      if (s_exit) break;
-      if (tid == 0) __nanosleep(backoff);
-      backoff = backoff < 256 ? backoff * 2 : 256;
-      __syncthreads();
-      continue;
-    }
-    backoff = 32;
-    const Act t = s_act;
-    const int l = t.sub;
-    const SubGeo& g = A.geo[l];
-    Acc acc{0u, 0u, 0.0, 0.0};
-    dispatch_item<DIM, P2>(A, g, t, s_item, sY, acc);
-    // CTA reductions of the item
-    const int any = __syncthreads_or(acc.flag);
-    const int anynf = __syncthreads_or(acc.nonfin);
-    unsigned long long emax = 0ull;
-    if (t.mode == M_FINAL)
-      emax = block_max_u64((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
-    double psum = 0.0;
-    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
-    if (sums) psum = block_sum2(acc.psum, sh_sum);
-    if (tid == 0) {
-      DevCtl* gc = A.ctl + l;
-      if (sums) __stcg(A.part + A.poff[l] + s_item, psum);
-      unsigned bits = 0;
-      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
-      if (anynf) bits |= 4u;
-      if (bits) atomicOr(&gc->acc_flags, bits);
-      if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
-      __threadfence();
-      const unsigned d = atomicAdd(&gc->done, 1u);
-      s_last = d == (unsigned)g.nitems - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      double sum = 0.0;
-      if (sums) {   // fixed-order reduction of the item partials (deterministic)
-        double v = 0.0;
-        for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
-        sum = block_sum2(v, sh_sum);
-      }
-      if (threadIdx.y == 0) {   // warp 0: controller state in/out in parallel
-        DevCtl* gc = A.ctl + l;
-        constexpr int NW = (int)(sizeof(DevCtl) / 8);
-        constexpr int WI = (int)(offsetof(DevCtl, word) / 8);
-        long long* sc = reinterpret_cast<long long*>(&s_ctl);
-        const long long* gsrc = reinterpret_cast<const long long*>(gc);
-        for (int i = threadIdx.x; i < NW; i += 32) sc[i] = __ldcg(gsrc + i);
-        __syncwarp();
-        bool more = false;
-        unsigned long long seq = 0;
-        if (threadIdx.x == 0) {
-          d_complete(A, s_ctl, l, sum, g.nodes);
-          seq = (s_ctl.word >> 32) + 1;
-          more = d_next_action(A, s_ctl);
-          s_ctl.acc_flags = 0;
-          s_ctl.acc_emax = 0ull;
-          s_ctl.done = 0;
-          if (!more) {
-            unsigned long long now;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            s_ctl.t_done = now;
-          }
-        }
-        __syncwarp();
-        long long* gdst = reinterpret_cast<long long*>(gc);
-        for (int i = threadIdx.x; i < NW; i += 32)
-          if (i != WI) __stcg(gdst + i, sc[i]);
-        __syncwarp();
-        if (threadIdx.x == 0) {
-          __threadfence();
-          if (more) {
-            atomicExch(&gc->word, seq << 32);
-          } else {
-            atomicExch(&gc->word, (seq << 32) | kDoneLow);
-            atomicAdd(A.n_done, 1u);
-          }
-        }
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -1277,7 +874,7 @@ __device__ __forceinline__ void claim(const WinArgs& A, int chunk, int& got, int
     if (q < A.nact) {
       l = A.act[q];
       const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
-      claimable = (unsigned)(w & 0xffffffffull) < (unsigned)A.geo[l].nitems;
+      claimable = w_cursor(w) < w_ntasks(w);
     }
     unsigned mask = __ballot_sync(0xffffffffu, claimable);
     while (mask != 0u && got < 0) {
@@ -1286,8 +883,8 @@ __device__ __forceinline__ void claim(const WinArgs& A, int chunk, int& got, int
       int it = -1, n = 0;
       if (lane == src) {
         const unsigned long long w2 = atomicAdd(&A.ctl[l].word, (unsigned long long)chunk);
-        const unsigned u = (unsigned)(w2 & 0xffffffffull);
-        const unsigned ni = (unsigned)A.geo[l].nitems;
+        const unsigned u = w_cursor(w2);
+        const unsigned ni = w_ntasks(w2);
         if (u < ni) {
           it = (int)u;
           n = (int)(ni - u < (unsigned)chunk ? ni - u : (unsigned)chunk);
@@ -1337,8 +934,8 @@ __device__ void decide(const WinArgs& A, int l, const SubGeo& g, double sum, Dev
   unsigned long long seq = 0;
   if (threadIdx.x == 0) {
     d_complete(A, s_ctl, l, sum, g.nodes);
-    seq = (s_ctl.word >> 32) + 1;
-    more = d_next_action(A, s_ctl);
+    seq = w_seq(s_ctl.word) + 1;
+    more = d_next_action(A, s_ctl, g.nitems);
     s_ctl.acc_flags = 0;
     s_ctl.acc_emax = 0ull;
     s_ctl.done = 0;
@@ -1363,9 +960,9 @@ __device__ void decide(const WinArgs& A, int l, const SubGeo& g, double sum, Dev
       A.probe[(seq % (unsigned long long)A.probe_cap) * 4 + 0] = now;
     }
     if (more) {
-      atomicExch(&gc->word, seq << 32);
+      atomicExch(&gc->word, w_make(seq, (unsigned)s_ctl.a_ntasks));
     } else {
-      atomicExch(&gc->word, (seq << 32) | kDoneLow);
+      atomicExch(&gc->word, w_make(seq, 0u));
       atomicAdd(A.n_done, 1u);
     }
   }
@@ -1524,6 +1121,50 @@ __device__ __forceinline__ void issue3(const WinArgs& A, const SubGeo& g, const 
   cpa_commit();
 }
 
+__device__ __forceinline__ void tma3(void* dst, const void* tmap, int x, int y, int z,
+                                     unsigned long long* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(m))
+      : "memory");
+}
+
+// One thread: the TMA copies of one 3D item into stage `st` (the halo boxes
+// of y and the a field, 36 x (TY+2) x (IZ3+2) at (c0-2, r0-1, z0-1), and the
+// TX x TY x IZ3 centre boxes; zero fill outside the box), completion on `mbar`.
+template <int MODE, int YM>
+__device__ __forceinline__ void issue3_tma(const WinArgs& A, int l, const Act& t, int c0, int r0,
+                                           int z0, Stage3& st, unsigned long long* mbar) {
+  constexpr bool HAS_A = YM == YM_ADD || YM == YM_SCALED;
+  constexpr bool NEED_F0 = MODE == M_STAGE3 || MODE == M_STAGEN || MODE == M_FINAL ||
+                           MODE == M_POWER || MODE == M_POWER_SEED;
+  int fa = 0;
+  if constexpr (MODE == M_STAGE2) fa = TF_F0 + t.fi;
+  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) fa = TF_D0 + (t.j - 1) % 3;
+  if constexpr (MODE == M_FINAL) fa = TF_D0 + t.s % 3;
+  if constexpr (MODE == M_POWER) fa = TF_D0 + t.vin;
+  const char* tm = reinterpret_cast<const char*>(A.tmap) + (size_t)l * TF_N * 2 * 128;
+  auto map = [&](int f, int kind) { return tm + (f * 2 + kind) * 128; };
+  constexpr unsigned HALO = TD3 * TH3 * TW2 * 8, CEN = IZ3 * TY * TX * 8;
+  unsigned bytes = HALO;
+  if constexpr (HAS_A) bytes += HALO;
+  if constexpr (MODE != M_NORM) {
+    bytes += CEN;
+    if constexpr (NEED_F0) bytes += CEN;
+    if constexpr (MODE == M_STAGEN) bytes += CEN;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  mbar_expect(mbar, bytes);
+  tma3(st.ys, map(TF_Y0 + t.yi, 0), c0 - 2, r0 - 1, z0 - 1, mbar);
+  if constexpr (HAS_A) tma3(st.as, map(fa, 0), c0 - 2, r0 - 1, z0 - 1, mbar);
+  if constexpr (MODE != M_NORM) {
+    tma3(st.cm, map(TF_MR, 1), c0, r0, z0, mbar);
+    if constexpr (NEED_F0) tma3(st.cf, map(TF_F0 + t.fi, 1), c0, r0, z0, mbar);
+    if constexpr (MODE == M_STAGEN) tma3(st.cd, map(TF_D0 + (t.j - 2) % 3, 1), c0, r0, z0, mbar);
+  }
+}
+
 template <int YM, int YMG = YM>
 struct TileAcc3 {
   const Stage3* st;
@@ -1667,7 +1308,8 @@ __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, cons
 
 template <bool P2, int MODE, int YM>
 __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
-                       Stage3* stage, Acc& acc, double* sh_sum) {
+                       Stage3* stage, Acc& acc, double* sh_sum, unsigned long long* mbar,
+                       unsigned& phases) {
   constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
   auto origin = [&](int item, int& c0, int& r0, int& z0) {
     const int ix = item % g.items_x;
@@ -1676,18 +1318,37 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     r0 = (rest % g.items_y) * TY;
     z0 = (rest / g.items_y) * IZ3;
   };
+  // TMA (cp.async.bulk.tensor.3d) with mbarrier completion when the plan has
+  // 3D tensor maps; cp.async otherwise.  Stage (i+1)&1 is refilled only after
+  // the CTA barrier that ends item i-1.
+  const bool tma = A.tmap != nullptr;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   int c0, r0, z0, nc0 = 0, nr0 = 0, nz0 = 0;
   origin(it0, c0, r0, z0);
-  issue3<MODE, YM>(A, g, t, c0, r0, z0, stage[0]);
+  if (tma) {
+    if (lead) issue3_tma<MODE, YM>(A, t.sub, t, c0, r0, z0, stage[0], &mbar[0]);
+  } else {
+    issue3<MODE, YM>(A, g, t, c0, r0, z0, stage[0]);
+  }
   for (int i = 0; i < nit; ++i) {
+    const int sb = i & 1;
     if (i + 1 < nit) {
       origin(it0 + i + 1, nc0, nr0, nz0);
-      issue3<MODE, YM>(A, g, t, nc0, nr0, nz0, stage[(i + 1) & 1]);
-      cpa_wait<1>();
-    } else {
+      if (tma) {
+        if (lead) issue3_tma<MODE, YM>(A, t.sub, t, nc0, nr0, nz0, stage[sb ^ 1], &mbar[sb ^ 1]);
+      } else {
+        issue3<MODE, YM>(A, g, t, nc0, nr0, nz0, stage[sb ^ 1]);
+        cpa_wait<1>();
+      }
+    } else if (!tma) {
       cpa_wait<0>();
     }
-    __syncthreads();
+    if (tma) {
+      mbar_wait(&mbar[sb], (phases >> sb) & 1u);
+      phases ^= 1u << sb;
+    } else {
+      __syncthreads();
+    }
     constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
     if constexpr (COMBINED) {
       Stage3& sg = stage[i & 1];
@@ -1714,17 +1375,20 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
 
 template <bool P2>
 __device__ void dispatch_chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
-                                Stage3* st, Acc& acc, double* sh) {
+                                Stage3* st, Acc& acc, double* sh, unsigned long long* mb,
+                                unsigned& ph) {
   switch (t.mode) {
-    case M_F0: chunk3<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_EULER: chunk3<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGE2: chunk3<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGE3: chunk3<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_STAGEN: chunk3<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_FINAL: chunk3<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_POWER: chunk3<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_POWER_SEED: chunk3<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh); break;
-    case M_NORM: chunk3<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh); break;
+    case M_F0: chunk3<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_EULER: chunk3<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGE2: chunk3<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGE3: chunk3<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_STAGEN: chunk3<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_FINAL: chunk3<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_POWER: chunk3<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
+    case M_POWER_SEED:
+      chunk3<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh, mb, ph);
+      break;
+    case M_NORM: chunk3<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, mb, ph); break;
     default: break;
   }
 }
@@ -1773,12 +1437,12 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
           // the previous action's data was written by other CTAs through the
           // generic proxy; the TMA loads of this chunk read it through the
           // async proxy (this thread issues them)
-          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          if (A.proxy_fence) asm volatile("fence.proxy.async.global;\n" ::: "memory");
           s_act = load_act(A, got);
           if (A.probe && got == A.probe_sub && it0 + nit == A.geo[got].nitems) {
             unsigned long long now;   // LAST chunk of the action claimed
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-            const unsigned long long sq = (*(volatile unsigned long long*)&A.ctl[got].word) >> 32;
+            const unsigned long long sq = w_seq(*(volatile unsigned long long*)&A.ctl[got].word);
             A.probe[(sq % (unsigned long long)A.probe_cap) * 4 + 1] = now;
           }
         }
@@ -1800,7 +1464,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
     Acc acc{0u, 0u, 0.0, 0.0};
     if constexpr (DIM == 2)
       dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_mbar, phases);
-    else dispatch_chunk3<P2>(A, g, t, it0, nit, stage, acc, sh_sum);
+    else dispatch_chunk3<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_mbar, phases);
     const int any = __syncthreads_or(acc.flag);
     const int anynf = __syncthreads_or(acc.nonfin);
     unsigned long long emax = 0ull;
@@ -1820,7 +1484,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
       if (s_last && A.probe && l == A.probe_sub) {
         unsigned long long now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        const unsigned long long sq = (*(volatile unsigned long long*)&gc->word) >> 32;
+        const unsigned long long sq = w_seq(*(volatile unsigned long long*)&gc->word);
         A.probe[(sq % (unsigned long long)A.probe_cap) * 4 + 2] = now;
       }
     }
@@ -1836,6 +1500,542 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
       if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
     }
     __syncthreads();
+  }
+}
+
+// ============================================================================
+// Dataflow 2D window kernel (k_windowD).
+//
+// An RKC2 step of a subdomain (stages 2..s and the final evaluation,
+// integrate.py:163-178) is published as ONE action, M_SWEEP, of s * nitems
+// tasks (level, item), level = j - 2.  Stage j at an item reads the stage
+// j-1 increments only in the item and its 8 neighbours (the 9-point stencil
+// of pma.py:87-149), so no stage needs a barrier over the whole box: a task
+// of level L in item row r is ready once rows r-1..r+1 completed level L-1,
+// which the per-row counters rowprog[] record (every completed sweep task
+// adds 1 to its row).  The 3-slot d ring of the stage recurrence stays safe
+// under that rule: the task that overwrites d_{j-2} at an item runs after
+// level j-1 completed in its rows and level j-2 completed two rows around.
+// The controller (accept/reject, error norm, sigma) still runs once per step,
+// when the last task of the sweep completes.  Levels of one subdomain thus
+// pipeline like a wavefront, and a single straggling subdomain keeps the
+// whole GPU busy (its tail used to run stage by stage on a few CTAs).
+//
+// Inside a CTA nothing waits on a CTA-wide barrier: warp 0 lane 0 claims
+// tasks and streams their tiles with TMA into a 2-deep ring of stages, each
+// slot carrying its task descriptor; every warp computes its rows of the
+// item, folds its flags / error ratio / partial sum into the slot and counts
+// itself done with a CTA-scope acquire-release atomic; the warp that
+// completes an item publishes it (row counter, action completion) and, when
+// it completes an action, runs the controller (decide) on its own -- the
+// other warps keep streaming.  Warp 0 only blocks waiting for work when it
+// has consumed every item it issued, so a task it waits for can never be one
+// its own CTA still has to compute.
+//
+// Per-node arithmetic (compute2_int / compute2) and every reduction order are
+// those of k_windowP, so both kernels give bitwise identical results.
+// ============================================================================
+
+constexpr int NBD = 2;                // ring depth of k_windowD
+constexpr int NWD = NT / 32;          // warps per CTA
+constexpr int M_EXIT = 99;            // ring-slot marker: no more work
+
+struct SlotD {                        // the task whose tiles occupy stage[b]
+  Act t;
+  int item, batch;
+  unsigned cnt;                       // warps done with the item (CTA-scope atomic)
+  unsigned wflag[NWD];                // per warp: bit0 flag, bit2 non-finite ratio
+  unsigned long long wemax[NWD];      // per warp: max error ratio (FINAL)
+  double wpsum[NWD];                  // per warp: partial sum (NORM / POWER)
+};
+
+// Completion accounting is batched: consecutive tasks of one claimed chunk
+// that share an item row (same cell of a sweep) form a batch; the warp that
+// completes a batch's last item publishes the whole batch with one fence and
+// one atomic per counter (row progress, action completion).
+constexpr int NBB = 4;                // batch records (>= NBD + 2: see issue_next_d)
+struct BatchD {
+  int sub, row, sweep, ntasks;
+  int size, final_, pad0, pad1;
+  unsigned done;                      // items completed (CTA-scope atomic)
+  unsigned flags;                     // ctl acc_flags bits of the batch's items
+  unsigned long long emax;            // max error ratio (FINAL items)
+  volatile int busy;                  // open: set by the issuer, cleared by the flusher
+};
+
+struct QueueD {                       // issuer state (warp 0 lane 0)
+  int sub, next, end, issued;         // claimed tasks [next, end) of subdomain sub
+  int bleft, bcur, nbatch, fence;     // open batch: items still to issue, record, count;
+                                      // fence: acquire + proxy fence due before the next TMA
+  int lock;                           // the ring filler's lock (one warp at a time)
+  int nfold;                          // items completed and published by their last warp
+  int mode, ntasks, nitems, ipr, nrows;
+  int kr_sub, kr_row, kr_lev;         // known: levels < kr_lev complete around kr_row
+  unsigned long long sbase, kr_base;
+  double h;
+  Act base;                           // the claimed action (yi, fi, s, c, h04, ...)
+};
+
+__device__ __forceinline__ unsigned atom_add_acqrel_cta(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(smem_u32(p)), "r"(v)
+               : "memory");
+  return old;
+}
+
+__device__ __forceinline__ bool mbar_test(unsigned long long* m, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void issue_any2(const WinArgs& A, const Act& t, int c0, int r0,
+                                           Stage2& st, unsigned long long* mb) {
+  switch (t.mode) {
+    case M_F0: issue2_tma<M_F0, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_EULER: issue2_tma<M_EULER, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGE2: issue2_tma<M_STAGE2, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGE3: issue2_tma<M_STAGE3, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_STAGEN: issue2_tma<M_STAGEN, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_FINAL: issue2_tma<M_FINAL, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_POWER: issue2_tma<M_POWER, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
+    case M_POWER_SEED: issue2_tma<M_POWER_SEED, YM_SEED>(A, t.sub, t, c0, r0, st, mb); break;
+    default: issue2_tma<M_NORM, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
+  }
+}
+
+// Sweep tasks are enumerated level-major (task = level * nitems + item):
+// with readiness-aware claiming, level L+1 starts in the first item rows as
+// soon as their neighbourhood completed level L, so consecutive levels of one
+// subdomain overlap by most of a level.
+// Readiness of sweep task tau of subdomain l (rows row-1..row+1 completed
+// level lev-1); returns the number of levels completed around the row.
+__device__ __forceinline__ long long sweep_levels_done(const WinArgs& A, const SubGeo& g, int row,
+                                                       unsigned long long sbase) {
+  const int r0 = row > 0 ? row - 1 : 0;
+  const int r1 = row + 1 < g.nrows ? row + 1 : g.nrows - 1;
+  const unsigned long long* rp = A.rowprog + g.rowoff;
+  unsigned long long m = ~0ull;
+  for (int r = r0; r <= r1; ++r) {
+    const unsigned long long v = *(volatile const unsigned long long*)(rp + r);
+    m = v < m ? v : m;
+  }
+  return m >= sbase ? (long long)((m - sbase) / (unsigned long long)g.ipr) : 0;
+}
+
+// Claim (warp 0, k_windowD): like claim(), but a sweep is only claimed when
+// the task at its cursor is ready, so CTAs spread over the subdomains'
+// ready wavefronts instead of queueing behind one.  The readiness test is a
+// heuristic (the cursor may move before the atomic): the claimed task may
+// still have to wait, briefly.
+__device__ __forceinline__ void claim_d(const WinArgs& A, int chunk, int& got, int& it0, int& nit) {
+  const int lane = threadIdx.x;
+  got = -1;
+  it0 = 0;
+  nit = 0;
+  for (int base = 0; base < A.nact && got < 0; base += 32) {
+    const int q = base + lane;
+    int l = -1;
+    bool ready = false;
+    if (q < A.nact) {
+      l = A.act[q];
+      const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
+      const unsigned cur = w_cursor(w);
+      ready = cur < w_ntasks(w);
+      const DevCtl* gc = A.ctl + l;
+      if (ready && *(volatile const int*)&gc->a_mode == M_SWEEP) {
+        const SubGeo& g = A.geo[l];
+        const int S = *(volatile const int*)&gc->a_s;
+        const unsigned long long sb = *(volatile const unsigned long long*)&gc->a_sbase;
+        const int ipr = __ldg(&g.ipr), R = __ldg(&g.nrows);
+        const int ni = __ldg(&g.nitems);
+        const int lev = (int)(cur / (unsigned)ni);
+        const int row = (int)(cur - (unsigned)lev * (unsigned)ni) / ipr;
+        (void)S;
+        (void)R;
+        if (lev >= 1) ready = sweep_levels_done(A, g, row, sb) >= lev;
+      }
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, ready);
+    while (mask != 0u && got < 0) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      int it = -1, n = 0;
+      if (lane == src) {
+        const unsigned long long w2 = atomicAdd(&A.ctl[l].word, (unsigned long long)chunk);
+        const unsigned u = w_cursor(w2);
+        const unsigned ni = w_ntasks(w2);
+        if (u < ni) {
+          it = (int)u;
+          n = (int)(ni - u < (unsigned)chunk ? ni - u : (unsigned)chunk);
+        }
+      }
+      it = __shfl_sync(0xffffffffu, it, src);
+      n = __shfl_sync(0xffffffffu, n, src);
+      if (it >= 0) {
+        got = __shfl_sync(0xffffffffu, l, src);
+        it0 = it;
+        nit = n;
+      }
+    }
+  }
+}
+
+// Fill the ring (one warp; called by whichever warp completed an item, so the
+// issuing latency -- claims, readiness polls, fences -- lands on a warp that
+// has a whole item of slack).  Issues in order while the next slot is free
+// and the front task is ready.  It may WAIT (for work, for readiness) only
+// when every issued item of this CTA has been completed and published
+// (nfold == issued): a task can then never depend on work this CTA still
+// holds, and the waiting cannot deadlock (tasks are claimed in cursor order
+// and a CTA's queue holds one subdomain's chunk).  Otherwise it returns and
+// the warp completing the next pending item tries again.
+__device__ void fill_ring_d(const WinArgs& A, QueueD& q, SlotD* slot, BatchD* bat, Stage2* stage,
+                            unsigned long long* full, unsigned long long* empty) {
+  const int lane = threadIdx.x;
+  if (lane == 0)
+    while (atomicCAS(&q.lock, 0, 1) != 0) __nanosleep(32);
+  __syncwarp();
+  unsigned backoff = 64;
+  while (true) {
+    const int n = __shfl_sync(0xffffffffu, lane == 0 ? q.issued : 0, 0);
+    const int b = n % NBD;
+    const unsigned u = (unsigned)(n / NBD);
+    int idle = 0;   // nothing of this CTA pending: waiting is allowed
+    if (lane == 0) idle = *(volatile int*)&q.nfold == n;
+    idle = __shfl_sync(0xffffffffu, idle, 0);
+    // ---- the slot: its previous item consumed by every warp
+    if (u >= 1) {
+      int ok = 0;
+      if (lane == 0) ok = mbar_test(&empty[b], (u - 1) & 1u) ? 1 : 0;
+      if (!__shfl_sync(0xffffffffu, ok, 0)) break;   // that item's completion retries
+    }
+    // ---- a claimed task
+    int have = __shfl_sync(0xffffffffu, (q.sub >= 0 && q.next < q.end) ? 1 : 0, 0);
+    if (!have) {
+      const unsigned nd = *(volatile unsigned*)A.n_done;
+      const int chunk = (A.nact - (int)nd) >= A.tail_n ? A.chunk_bulk : A.chunk_tail;
+      int got, it0, nit;
+      claim_d(A, chunk, got, it0, nit);
+      if (got < 0) {
+        if (!idle) break;
+        int ex = 0;
+        if (lane == 0) ex = *(volatile unsigned*)A.n_done >= (unsigned)A.nact;
+        ex = __shfl_sync(0xffffffffu, ex, 0);
+        if (ex) {   // every subdomain finished its window: the exit marker
+          if (lane == 0) {
+            slot[b].t.mode = M_EXIT;
+            mbar_arrive(&full[b]);   // release: the marker
+            ++q.issued;
+          }
+          break;
+        }
+        if (lane == 0) __nanosleep(backoff);
+        backoff = backoff < 1024 ? 2 * backoff : 1024;
+        __syncwarp();
+        continue;
+      }
+      if (lane == 0) {
+        __threadfence();   // acquire: the action and the data of the previous action
+        const DevCtl* gc = A.ctl + got;
+        q.base = load_act(A, got);
+        q.mode = q.base.mode;
+        q.ntasks = __ldcg(&gc->a_ntasks);
+        q.h = __ldcg(&gc->a_h);
+        q.sbase = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(&gc->a_sbase));
+        const SubGeo& g = A.geo[got];
+        q.nitems = g.nitems;
+        q.ipr = g.ipr;
+        q.nrows = g.nrows;
+        q.sub = got;
+        q.next = it0;
+        q.end = it0 + nit;
+        q.fence = 1;
+      }
+      __syncwarp();
+    }
+    // ---- the front task: readiness, then issue (lane 0)
+    int state = 0;   // 1 issued, 0 not ready
+    if (lane == 0) {
+      const int tau = q.next;
+      int lev = 0, item = tau;
+      if (q.mode == M_SWEEP) {
+        lev = tau / q.nitems;
+        item = tau - lev * q.nitems;
+      }
+      const int row = item / q.ipr;
+      bool ready = true;
+      if (q.mode == M_SWEEP && lev >= 1) {
+        const bool known = q.kr_sub == q.sub && q.kr_row == row && q.kr_base == q.sbase &&
+                           lev <= q.kr_lev;
+        if (!known) {
+          q.fence = 1;   // new counter values observed: acquire before the TMA reads
+          const long long L = sweep_levels_done(A, A.geo[q.sub], row, q.sbase);
+          q.kr_sub = q.sub;
+          q.kr_row = row;
+          q.kr_base = q.sbase;
+          q.kr_lev = (int)(L < (1 << 30) ? L : (1 << 30));
+          ready = lev <= q.kr_lev;
+        }
+      }
+      if (ready) {
+        Act t = q.base;
+        if (q.mode == M_SWEEP) {
+          const int j = lev + 2;
+          const int s = t.s;
+          if (j <= s) {
+            const int base = A.coef_off[s];
+            t.mode = j == 2 ? M_STAGE2 : (j == 3 ? M_STAGE3 : M_STAGEN);
+            t.j = j;
+            t.mu = A.coef[4 * (base + j) + 0];
+            t.nu = A.coef[4 * (base + j) + 1];
+            t.hmut = q.h * A.coef[4 * (base + j) + 2];
+            t.hgt = q.h * A.coef[4 * (base + j) + 3];
+          } else {
+            t.mode = M_FINAL;
+          }
+        }
+        if (q.bleft == 0) {   // open a batch: the rest of this item row / chunk
+          const int nb = q.nbatch % NBB;
+          while (bat[nb].busy) __nanosleep(32);   // its flusher needs nothing from us
+          __threadfence_block();
+          BatchD& bt = bat[nb];
+          int size = q.end - tau;
+          if (q.mode == M_SWEEP) size = min(size, (row + 1) * q.ipr - item);
+          bt.sub = q.sub;
+          bt.row = row;
+          bt.sweep = q.mode == M_SWEEP ? 1 : 0;
+          bt.ntasks = q.ntasks;
+          bt.size = size;
+          bt.final_ = t.mode == M_FINAL ? 1 : 0;
+          bt.done = 0u;
+          bt.flags = 0u;
+          bt.emax = 0ull;
+          bt.busy = 1;
+          q.bleft = size;
+          q.bcur = nb;
+          ++q.nbatch;
+        }
+        --q.bleft;
+        SlotD& sd = slot[b];
+        sd.t = t;
+        sd.item = item;
+        sd.batch = q.bcur;
+        if (q.fence) {   // once per claim / fresh readiness observation
+          __threadfence();   // acquire side of the readiness counters
+          if (A.proxy_fence) asm volatile("fence.proxy.async.global;\n" ::: "memory");   // generic writes -> TMA reads
+          q.fence = 0;
+        }
+        const SubGeo& g = A.geo[q.sub];
+        const int ix = item % g.items_x, iy = item / g.items_x;
+        issue_any2(A, t, ix * TX, iy * IR2, stage[b], &full[b]);
+        ++q.issued;
+        ++q.next;
+        state = 1;
+      }
+    }
+    state = __shfl_sync(0xffffffffu, state, 0);
+    if (state == 1) continue;
+    if (!idle) break;
+    if (lane == 0) __nanosleep(backoff);
+    backoff = backoff < 1024 ? 2 * backoff : 1024;
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane == 0) atomicExch(&q.lock, 0);
+}
+
+// Fixed-order sum of the per-item partials of an action by one warp, in
+// exactly block_sum's order over NT threads (k_windowP): thread t sums items
+// t, t+NT, ..., each warp reduces its 32 values by the shuffle tree, the
+// warp totals are added in warp order.
+__device__ double warp_items_sum(const double* part, int n) {
+  double tot = 0.0;
+#pragma unroll 1
+  for (int w = 0; w < NWD; ++w) {
+    double v = 0.0;
+    for (int i = w * 32 + (int)threadIdx.x; i < n; i += NT) v += __ldcg(part + i);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    tot = w == 0 ? v : tot + v;
+  }
+  return __shfl_sync(0xffffffffu, tot, 0);
+}
+
+template <bool P2, int MODE, int YM>
+__device__ __forceinline__ void item_d(const WinArgs& A, const SubGeo& g, const Act& t, int item,
+                                       const Stage2& st, Acc& acc, double& ps) {
+  constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
+  const int n0 = g.n[0], n1 = g.n[1], items_x = g.items_x;
+  const long long pitch = g.pitch;
+  const int ix = item % items_x, iy = item / items_x;
+  const int c0 = ix * TX, r0 = iy * IR2;
+  const long long kb = g.off + (long long)r0 * pitch + c0 + threadIdx.x;
+  if constexpr (SUMS) {
+    compute2<P2, MODE, YM>(A, g, t, c0, r0, st, acc, &ps);
+  } else if (r0 >= 1 && r0 + IR2 <= n0 - 1 && c0 >= 1 && c0 + TX <= n1 - 1) {
+    compute2_int<P2, MODE, YM, false>(A, g, t, kb, pitch, r0, c0, n0, n1, st, acc);
+  } else {
+    compute2_int<P2, MODE, YM, true>(A, g, t, kb, pitch, r0, c0, n0, n1, st, acc);
+  }
+}
+
+template <bool P2>
+__device__ __forceinline__ void dispatch_item_d(const WinArgs& A, const SubGeo& g, const Act& t,
+                                                int item, const Stage2& st, Acc& acc, double& ps) {
+  switch (t.mode) {
+    case M_F0: item_d<P2, M_F0, YM_PLAIN>(A, g, t, item, st, acc, ps); break;
+    case M_EULER: item_d<P2, M_EULER, YM_PLAIN>(A, g, t, item, st, acc, ps); break;
+    case M_STAGE2: item_d<P2, M_STAGE2, YM_SCALED>(A, g, t, item, st, acc, ps); break;
+    case M_STAGE3: item_d<P2, M_STAGE3, YM_ADD>(A, g, t, item, st, acc, ps); break;
+    case M_STAGEN: item_d<P2, M_STAGEN, YM_ADD>(A, g, t, item, st, acc, ps); break;
+    case M_FINAL: item_d<P2, M_FINAL, YM_ADD>(A, g, t, item, st, acc, ps); break;
+    case M_POWER: item_d<P2, M_POWER, YM_SCALED>(A, g, t, item, st, acc, ps); break;
+    case M_POWER_SEED: item_d<P2, M_POWER_SEED, YM_SEED>(A, g, t, item, st, acc, ps); break;
+    case M_NORM: item_d<P2, M_NORM, YM_PLAIN>(A, g, t, item, st, acc, ps); break;
+    default: break;
+  }
+}
+
+// Batch completion (one warp): publish its items with one fence and one atomic
+// per counter; the warp completing an action runs its controller (decide).
+template <bool P2>
+__device__ __noinline__ void publish_batch_d(const WinArgs& A, BatchD* s_bat, int bi, const Act& t,
+                                             int l, const SubGeo& g, DevCtl& ctlw) {
+    const int lane = threadIdx.x;
+    int done_act = 0;
+    if (lane == 0) {
+      BatchD& bt = s_bat[bi];
+      const int size = bt.size, row = bt.row, sweep = bt.sweep, ntasks = bt.ntasks;
+      const unsigned gb = bt.flags;
+      const unsigned long long emax = bt.emax;
+      const bool final_ = bt.final_ != 0;
+      __threadfence_block();
+      bt.busy = 0;   // the record is free again
+      DevCtl* gc = A.ctl + l;
+      if (gb) atomicOr(&gc->acc_flags, gb);
+      if (final_) atomicMax(&gc->acc_emax, emax);
+      __threadfence();   // release: the batch's outputs before its counters
+      if (sweep) atomicAdd(A.rowprog + g.rowoff + row, (unsigned long long)size);
+      const unsigned d = atomicAdd(&gc->done, (unsigned)size);
+      done_act = d + (unsigned)size == (unsigned)ntasks;
+    }
+    done_act = __shfl_sync(0xffffffffu, done_act, 0);
+    if (done_act) {
+      __threadfence();   // acquire: every task's partials / accumulators
+      double sum = 0.0;
+      if (t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM)
+        sum = warp_items_sum(A.part + A.poff[l], g.nitems);
+      decide(A, l, g, sum, ctlw);
+    }
+}
+
+template <bool P2>
+__global__ void __launch_bounds__(NT, DDPMA_MINB2) k_windowD(const WinArgs A) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Stage2* stage = reinterpret_cast<Stage2*>(
+      dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
+  __shared__ __align__(8) unsigned long long s_full[NBD], s_empty[NBD];
+  __shared__ SlotD s_slot[NBD];
+  __shared__ BatchD s_bat[NBB];
+  __shared__ QueueD s_q;
+  __shared__ DevCtl s_ctlw[NWD];      // per-warp controller scratch (decide)
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  if (lane == 0 && warp == 0) {
+    for (int b = 0; b < NBD; ++b) {
+      mbar_init(&s_full[b]);
+      mbar_init_n(&s_empty[b], NWD);
+      s_slot[b].cnt = 0;
+    }
+    for (int b = 0; b < NBB; ++b) s_bat[b].busy = 0;
+    s_q.sub = -1;
+    s_q.next = s_q.end = 0;
+    s_q.issued = 0;
+    s_q.bleft = 0;
+    s_q.nbatch = 0;
+    s_q.kr_sub = -1;
+    s_q.fence = 1;
+    s_q.lock = 0;
+    s_q.nfold = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = warp * TX + lane; i < 97 * 3; i += NT) (&s_logtab[0][0])[i] = (&kLogTabD[0][0])[i];
+  __syncthreads();
+
+  if (warp == 0) fill_ring_d(A, s_q, s_slot, s_bat, stage, s_full, s_empty);
+  int k = 0;   // items consumed by this warp
+  while (true) {
+    const int b = k % NBD;
+    mbar_wait(&s_full[b], (unsigned)(k / NBD) & 1u);
+    SlotD& sd = s_slot[b];
+    const Act t = sd.t;
+    if (t.mode == M_EXIT) break;
+    const int item = sd.item;
+    const int l = t.sub;
+    const SubGeo& g = A.geo[l];
+    Acc acc{0u, 0u, 0.0, 0.0};
+    double ps = 0.0;
+    dispatch_item_d<P2>(A, g, t, item, stage[b], acc, ps);
+    // per-warp fold of the item's flags / error ratio / partial sum
+    const unsigned fl = __any_sync(0xffffffffu, acc.flag != 0u) ? 1u : 0u;
+    const unsigned nf = __any_sync(0xffffffffu, acc.nonfin != 0u) ? 4u : 0u;
+    unsigned long long em = (unsigned long long)__double_as_longlong(acc.ratio);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_down_sync(0xffffffffu, em, off);
+      em = o > em ? o : em;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ps += __shfl_down_sync(0xffffffffu, ps, off);
+    int last = 0;
+    if (lane == 0) {
+      sd.wflag[warp] = fl | nf;
+      sd.wemax[warp] = em;
+      sd.wpsum[warp] = ps;
+    }
+    __syncwarp();   // every lane's global stores of the item precede lane 0's release
+    if (lane == 0) last = atom_add_acqrel_cta(&sd.cnt, 1u) == (unsigned)(NWD - 1);
+    last = __shfl_sync(0xffffffffu, last, 0);
+    // the warp completing the item folds it into its batch, then frees the slot
+    int flush = 0, bi = 0;
+    if (last && lane == 0) {
+      unsigned bits = 0;
+      unsigned long long emax = 0ull;
+      double psum = 0.0;
+      for (int w = 0; w < NWD; ++w) {
+        bits |= sd.wflag[w];
+        emax = sd.wemax[w] > emax ? sd.wemax[w] : emax;
+        psum = w == 0 ? sd.wpsum[0] : psum + sd.wpsum[w];   // block_sum's order
+      }
+      bi = sd.batch;
+      sd.cnt = 0;
+      BatchD& bt = s_bat[bi];
+      const bool final_ = t.mode == M_FINAL;
+      unsigned gb = 0;
+      if (bits & 1u) gb |= final_ ? 2u : 1u;
+      if (bits & 4u) gb |= 4u;
+      if (gb) atomicOr(&bt.flags, gb);
+      if (final_) atomicMax(&bt.emax, emax);
+      if (t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM)
+        __stcg(A.part + A.poff[l] + item, psum);
+      flush = atom_add_acqrel_cta(&bt.done, 1u) + 1u == (unsigned)bt.size;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[b]);   // this warp is done with stage b
+    ++k;
+    flush = __shfl_sync(0xffffffffu, flush, 0);
+    if (flush) publish_batch_d<P2>(A, s_bat, bi, t, l, g, s_ctlw[warp]);
+    // the item is completed and published: this warp refills the ring
+    if (lane == 0) atomicAdd(&s_q.nfold, 1);
+    __syncwarp();
+    fill_ring_d(A, s_q, s_slot, s_bat, stage, s_full, s_empty);
   }
 }
 
@@ -1856,308 +2056,36 @@ __global__ void k_window_begin(const WinArgs A) {
   } else {
     c.phase = P_F0;
   }
-  c.word = (c.word & 0xffffffff00000000ull);
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c.t_begin));
-  d_publish(A, c, gc);
-}
-
-// ============================================================================
-// Warp-specialised 2D window kernel (k_windowW): 8 consumer warps + 1
-// producer warp per CTA.
-//
-// The producer warp claims chunks (claim-ahead: the next chunk is claimed
-// while the consumers still work on the current one), publishes each chunk's
-// action through a 2-slot mailbox (mbarriers cfull / cempty) and streams every
-// item's tiles into an NS-deep ring of shared-memory stages with TMA (full[b]:
-// transaction bytes; empty[b]: one arrival per consumer warp).  Consumers
-// never meet the producer at a barrier; among themselves they synchronise
-// only at chunk ends (named barrier 1) for the flag / error-ratio reductions
-// and the completion accounting.  The per-item arithmetic is compute2_int /
-// compute2 (bitwise identical to the other window kernels).
-// ============================================================================
-
-constexpr int NS2 = 3;                 // ring depth (stages) of k_windowW
-constexpr int NTW = NT + 32;           // threads per CTA of k_windowW
-
-__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
-__device__ __forceinline__ int cbar_or(int p) {
-  int r;
-  asm volatile(
-      "{\n .reg .pred pi, po;\n setp.ne.s32 pi, %1, 0;\n"
-      " bar.red.or.pred po, 1, 256, pi;\n selp.s32 %0, 1, 0, po;\n}\n"
-      : "=r"(r)
-      : "r"(p)
-      : "memory");
-  return r;
-}
-__device__ __forceinline__ double csum(double v, double* sh) {   // block_sum over consumers
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-  if (threadIdx.x == 0) sh[threadIdx.y] = v;
-  cbar();
-  double tot = 0.0;
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    tot = sh[0];
-    for (int w = 1; w < NT / 32; ++w) tot += sh[w];
-  }
-  cbar();
-  return tot;
-}
-__device__ __forceinline__ unsigned long long cmax(unsigned long long v, unsigned long long* sh) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned long long o = __shfl_down_sync(0xffffffffu, v, off);
-    v = o > v ? o : v;
-  }
-  if (threadIdx.x == 0) sh[threadIdx.y] = v;
-  cbar();
-  unsigned long long m = 0;
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    m = sh[0];
-    for (int w = 1; w < NT / 32; ++w) m = sh[w] > m ? sh[w] : m;
-  }
-  cbar();
-  return m;
-}
-
-// Producer side: the TMA copies of one item for a runtime mode.
-__device__ __forceinline__ void issue_any2(const WinArgs& A, const Act& t, int c0, int r0,
-                                           Stage2& st, unsigned long long* mb) {
-  switch (t.mode) {
-    case M_F0: issue2_tma<M_F0, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_EULER: issue2_tma<M_EULER, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_STAGE2: issue2_tma<M_STAGE2, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_STAGE3: issue2_tma<M_STAGE3, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_STAGEN: issue2_tma<M_STAGEN, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_FINAL: issue2_tma<M_FINAL, YM_ADD>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_POWER: issue2_tma<M_POWER, YM_SCALED>(A, t.sub, t, c0, r0, st, mb); break;
-    case M_POWER_SEED: issue2_tma<M_POWER_SEED, YM_SEED>(A, t.sub, t, c0, r0, st, mb); break;
-    default: issue2_tma<M_NORM, YM_PLAIN>(A, t.sub, t, c0, r0, st, mb); break;
-  }
-}
-
-// Consumer side of one chunk: n = ring position (items consumed so far).
-template <bool P2, int MODE, int YM>
-__device__ void cchunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0, int nit,
-                        Stage2* stage, Acc& acc, double* sh_sum, unsigned long long* full,
-                        unsigned long long* empty, unsigned& n) {
-  constexpr bool SUMS = MODE == M_POWER || MODE == M_POWER_SEED || MODE == M_NORM;
-  const int n0 = __ldg(&g.n[0]), n1 = __ldg(&g.n[1]), items_x = __ldg(&g.items_x);
-  const long long pitch = __ldg(&g.pitch), goff = __ldg(&g.off);
-  int ix = it0 % items_x, iy = it0 / items_x;
-  for (int i = 0; i < nit; ++i, ++n) {
-    const unsigned b = n % NS2, u = n / NS2;
-    mbar_wait(&full[b], u & 1u);
-    double ps = 0.0;
-    const int c0 = ix * TX, r0 = iy * IR2;
-    const long long kb = goff + (long long)r0 * pitch + c0 + threadIdx.x;
-    if constexpr (SUMS) {
-      compute2<P2, MODE, YM>(A, g, t, c0, r0, stage[b], acc, &ps);
-    } else if (r0 >= 1 && r0 + IR2 <= n0 - 1 && c0 >= 1 && c0 + TX <= n1 - 1) {
-      compute2_int<P2, MODE, YM, false>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[b], acc);
-    } else {
-      compute2_int<P2, MODE, YM, true>(A, g, t, kb, pitch, r0, c0, n0, n1, stage[b], acc);
-    }
-    __syncwarp();
-    if (threadIdx.x == 0) mbar_arrive(&empty[b]);   // this warp is done with stage b
-    if (++ix == items_x) {
-      ix = 0;
-      ++iy;
-    }
-    if constexpr (SUMS) {
-      const double sv = csum(ps, sh_sum);   // per-item partial: deterministic
-      if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, sv);
-    }
-  }
-}
-
-template <bool P2>
-__device__ void dispatch_cchunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
-                                 int nit, Stage2* st, Acc& acc, double* sh,
-                                 unsigned long long* fu, unsigned long long* em, unsigned& n) {
-  switch (t.mode) {
-    case M_F0: cchunk2<P2, M_F0, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_EULER: cchunk2<P2, M_EULER, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_STAGE2: cchunk2<P2, M_STAGE2, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_STAGE3: cchunk2<P2, M_STAGE3, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_STAGEN: cchunk2<P2, M_STAGEN, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_FINAL: cchunk2<P2, M_FINAL, YM_ADD>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_POWER: cchunk2<P2, M_POWER, YM_SCALED>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    case M_POWER_SEED:
-      cchunk2<P2, M_POWER_SEED, YM_SEED>(A, g, t, it0, nit, st, acc, sh, fu, em, n);
-      break;
-    case M_NORM: cchunk2<P2, M_NORM, YM_PLAIN>(A, g, t, it0, nit, st, acc, sh, fu, em, n); break;
-    default: break;
-  }
-}
-
-struct ChunkSlot {
-  Act t;
-  int it0, nit, exit, pad;
-};
-
-template <bool P2>
-__global__ void __launch_bounds__(NTW, 3) k_windowW(const WinArgs A) {
-  extern __shared__ __align__(128) unsigned char dsm[];
-  Stage2* stage = reinterpret_cast<Stage2*>(
-      dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
-  __shared__ __align__(8) unsigned long long s_full[NS2], s_empty[NS2], s_cfull[2], s_cempty[2];
-  __shared__ ChunkSlot s_cs[2];
-  __shared__ double sh_sum[NT / 32];
-  __shared__ unsigned long long sh_max[NT / 32];
-  __shared__ DevCtl s_ctl;
-  __shared__ int s_last;
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    for (int b = 0; b < NS2; ++b) {
-      mbar_init(&s_full[b]);
-      mbar_init_n(&s_empty[b], NT / 32);
-    }
-    for (int k = 0; k < 2; ++k) {
-      mbar_init(&s_cfull[k]);
-      mbar_init(&s_cempty[k]);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int i = threadIdx.y * TX + threadIdx.x; i < 97 * 3; i += NTW)
-    (&s_logtab[0][0])[i] = (&kLogTabD[0][0])[i];
-  __syncthreads();
-
-  if (threadIdx.y == TY) {
-    // ---------------------------------------------------------- producer
-    const int lane = threadIdx.x;
-    unsigned n = 0;       // items issued
-    int k = 0;            // chunks published
-    unsigned backoff = 32;
-    while (true) {
-      const int slot = k & 1;
-      if (k >= 2) mbar_wait(&s_cempty[slot], ((k >> 1) - 1) & 1);
-      const unsigned nd = *(volatile unsigned*)A.n_done;
-      const int chunk = (A.nact - (int)nd) >= A.tail_n ? A.chunk_bulk : A.chunk_tail;
-      int got, it0, nit;
-      claim(A, chunk, got, it0, nit);
-      if (got < 0) {
-        if (*(volatile unsigned*)A.n_done >= (unsigned)A.nact) {
-          if (lane == 0) {
-            s_cs[slot].exit = 1;
-            mbar_arrive(&s_cfull[slot]);
-          }
-          break;
-        }
-        __nanosleep(backoff);
-        backoff = backoff < 256 ? backoff * 2 : 256;
-        continue;
-      }
-      backoff = 32;
-      if (lane == 0) {
-        __threadfence();   // acquire: the action and the data of the previous action
-        asm volatile("fence.proxy.async.global;\n" ::: "memory");   // generic writes -> TMA reads
-        const Act t = load_act(A, got);
-        s_cs[slot].t = t;
-        s_cs[slot].it0 = it0;
-        s_cs[slot].nit = nit;
-        s_cs[slot].exit = 0;
-        mbar_arrive(&s_cfull[slot]);
-        const int items_x = __ldg(&A.geo[got].items_x);
-        int ix = it0 % items_x, iy = it0 / items_x;
-        for (int i = 0; i < nit; ++i, ++n) {
-          const unsigned b = n % NS2, u = n / NS2;
-          if (u >= 1) mbar_wait(&s_empty[b], (u - 1) & 1u);
-          issue_any2(A, t, ix * TX, iy * IR2, stage[b], &s_full[b]);
-          if (++ix == items_x) {
-            ix = 0;
-            ++iy;
-          }
-        }
-      }
-      __syncwarp();
-      ++k;
-    }
-    return;
-  }
-
-  // ------------------------------------------------------------ consumers
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  unsigned n = 0;
-  int k = 0;
-  while (true) {
-    const int slot = k & 1;
-    mbar_wait(&s_cfull[slot], (k >> 1) & 1);
-    const int ex = s_cs[slot].exit;
-    // the action stays in the mailbox slot (read from shared memory where
-    // used) until the chunk is complete; the slot is released at chunk end
-    const Act& t = s_cs[slot].t;
-    const int it0 = s_cs[slot].it0, nit = s_cs[slot].nit;
-    ++k;
-    if (ex) break;
-    const int l = t.sub;
-    const SubGeo& g = A.geo[l];
-    Acc acc{0u, 0u, 0.0, 0.0};
-    dispatch_cchunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_full, s_empty, n);
-    const int any = cbar_or(acc.flag);
-    const int anynf = cbar_or(acc.nonfin);
-    unsigned long long emax = 0ull;
-    if (t.mode == M_FINAL)
-      emax = cmax((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
-    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
-    if (tid == 0) {
-      DevCtl* gc = A.ctl + l;
-      unsigned bits = 0;
-      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
-      if (anynf) bits |= 4u;
-      if (bits) atomicOr(&gc->acc_flags, bits);
-      if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
-      __threadfence();
-      const unsigned d = atomicAdd(&gc->done, (unsigned)nit);
-      s_last = d + (unsigned)nit == (unsigned)g.nitems;
-    }
-    cbar();
-    if (s_last) {
-      __threadfence();
-      double sum = 0.0;
-      if (sums) {
-        double v = 0.0;
-        for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
-        sum = csum(v, sh_sum);
-      }
-      if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
-    }
-    cbar();
-    if (tid == 0) mbar_arrive(&s_cempty[slot]);   // mailbox slot free
-  }
+  d_publish(A, c, gc, A.geo[l].nitems);
 }
 
 }  // namespace
 
-// DDPMA_WS=1 selects the warp-specialised 2D kernel k_windowW (default: the
-// single-role k_windowP, measured faster on C3: 4 vs 3 resident CTAs per SM).
-static bool window_ws() {
-  static const int ws = getenv("DDPMA_WS") ? atoi(getenv("DDPMA_WS")) : 0;
-  return ws != 0;
+
+// The dataflow kernel k_windowD runs 2D windows (default); DDPMA_KERNEL=P
+// selects the stage-by-stage kernel k_windowP (A/B comparisons: bitwise
+// identical results).  3D windows run k_windowP<3>.
+bool window_dataflow(int dim) {
+  static const bool p = getenv("DDPMA_KERNEL") && getenv("DDPMA_KERNEL")[0] == 'P';
+  return dim == 2 && !p;
+}
+
+static int smem_bytes(int dim) {
+  return dim == 2 ? 2 * STAGE2_BYTES + 128 : 2 * (int)sizeof(Stage3) + 128;
 }
 
 int window_blocks(int dim, int pow2) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (dim == 2 && window_ws()) {
-    const int smem = NS2 * STAGE2_BYTES + 128;
-    cudaFuncSetAttribute(k_windowW<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_windowW<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowW<true>, NTW, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowW<false>, NTW, smem);
-  } else if (dim == 2) {
-    const int smem = 2 * STAGE2_BYTES + 128;
-    cudaFuncSetAttribute(k_windowP<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_windowP<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, true>, NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<2, false>, NT, smem);
-  } else {
-    const int smem = 2 * (int)sizeof(Stage3) + 128;
-    cudaFuncSetAttribute(k_windowP<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_windowP<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (pow2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<3, true>, NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_windowP<3, false>, NT, smem);
-  }
+  const int smem = smem_bytes(dim);
+  const void* fn;
+  if (dim == 2 && window_dataflow(2)) fn = pow2 ? (const void*)k_windowD<true> : (const void*)k_windowD<false>;
+  else if (dim == 2) fn = pow2 ? (const void*)k_windowP<2, true> : (const void*)k_windowP<2, false>;
+  else fn = pow2 ? (const void*)k_windowP<3, true> : (const void*)k_windowP<3, false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, NT, smem);
   return sms * (per > 0 ? per : 1);
 }
 
@@ -2170,21 +2098,11 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   if (a.nact <= 0) return;
   const dim3 blk(TX, TY);
   void* args[] = {(void*)&a};
-  void* fn;
-  size_t smem = 0;
-  if (a.P.dim == 2 && window_ws() && a.tmap != nullptr) {
-    fn = a.P.pow2 ? (void*)k_windowW<true> : (void*)k_windowW<false>;
-    smem = NS2 * STAGE2_BYTES + 128;
-    cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(TX, TY + 1), args, smem, (cudaStream_t)stream);
-    return;
-  } else if (a.P.dim == 2) {
-    fn = a.P.pow2 ? (void*)k_windowP<2, true> : (void*)k_windowP<2, false>;
-    smem = 2 * STAGE2_BYTES + 128;
-  } else {
-    fn = a.P.pow2 ? (void*)k_windowP<3, true> : (void*)k_windowP<3, false>;
-    smem = 2 * sizeof(Stage3) + 128;
-  }
-  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem, (cudaStream_t)stream);
+  const void* fn;
+  if (a.P.dim == 2 && a.sweep) fn = a.P.pow2 ? (const void*)k_windowD<true> : (const void*)k_windowD<false>;
+  else if (a.P.dim == 2) fn = a.P.pow2 ? (const void*)k_windowP<2, true> : (const void*)k_windowP<2, false>;
+  else fn = a.P.pow2 ? (const void*)k_windowP<3, true> : (const void*)k_windowP<3, false>;
+  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem_bytes(a.P.dim), (cudaStream_t)stream);
 }
 
 }  // namespace ddpma

@@ -193,6 +193,8 @@ struct ddpma_plan {
   int win_blocks = 0;
   int chunk_bulk = 8, chunk_tail = 2, tail_n = 16;   // window scheduler knobs (parsed once)
   unsigned long long* d_probe = nullptr;             // DDPMA_PROBE timestamps (debug)
+  unsigned long long* d_rowprog = nullptr;           // k_windowD per-row task counters
+  long long total_rows = 0;
   bool host_ctl = false;
   bool integ_ready = false;                // ddpma_integrate_window: integrators initialised
   void* d_tmap = nullptr;                  // 2D TMA tensor maps (persist.cu issue2_tma)
@@ -863,6 +865,9 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   A.chunk_tail = p->chunk_tail;
   A.tail_n = p->tail_n;
   A.tmap = p->d_tmap;
+  A.sweep = (window_dataflow(p->dim) && p->d_tmap != nullptr) ? 1 : 0;
+  A.rowprog = p->d_rowprog;
+  A.proxy_fence = getenv("DDPMA_NO_PROXY_FENCE") ? 0 : 1;   // measurement knob only
   unsigned long long* d_probe = p->d_probe;
   const bool pe = d_probe != nullptr;
   if (pe) {
@@ -1289,6 +1294,7 @@ extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   cudaFree(p->d_trace);
   cudaFree(p->d_tmap);
   cudaFree(p->d_probe);
+  cudaFree(p->d_rowprog);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->st) cudaStreamDestroy(p->st);
   delete p;
@@ -1434,6 +1440,7 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   // geometry + arena
   long long off = 0;
   int tiles = 0;
+  long long nrows_total = 0;
   for (int l = 0; l < (int)p->local.size(); ++l) {
     const ddpma_subdomain& S = p->subs[p->local[l]];
     SubGeo g{};
@@ -1482,12 +1489,20 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
       g.items_z = (g.n[0] + IZ3 - 1) / IZ3;
     }
     g.nitems = g.items_x * g.items_y * g.items_z;
+    g.ipr = p->dim == 2 ? g.items_x : g.items_x * g.items_y;   // a row of items / a plane
+    g.nrows = g.nitems / g.ipr;
+    g.rowoff = nrows_total;
+    nrows_total += g.nrows;
     tiles += g.ntiles;
     p->geo.push_back(g);
   }
   p->arena = off;
   p->total_tiles = tiles;
+  p->total_rows = nrows_total;
   p->ctl.assign(p->local.size(), Ctl{});
+  p->sub_evals.assign(p->local.size(), 0);
+  p->last_evals.assign(p->local.size(), 0);
+  p->ctl_prev.assign(p->local.size(), DevCtl{});
   ddpma_status s = DDPMA_OK;
   auto fail = [&](cudaError_t e, const char* w) {
     set_global_error(std::string("CUDA error in ") + w + ": " + cudaGetErrorString(e));
@@ -1594,13 +1609,19 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
         return fail(ce, "trace");
     }
     p->win_blocks = window_blocks(p->dim, P.pow2);
+    if ((ce = cudaMalloc((void**)&p->d_rowprog, sizeof(unsigned long long) * std::max(1LL, p->total_rows))) != cudaSuccess)
+      return fail(ce, "rowprog");
+    if ((ce = cudaMemsetAsync(p->d_rowprog, 0, sizeof(unsigned long long) * std::max(1LL, p->total_rows), p->st)) != cudaSuccess)
+      return fail(ce, "rowprog memset");
     if (getenv("DDPMA_PROBE")) {
       if ((ce = cudaMalloc((void**)&p->d_probe, sizeof(unsigned long long) * 4 * (1 << 16))) != cudaSuccess)
         return fail(ce, "probe");
     }
-    if (p->dim == 2 && getenv("DDPMA_NO_TMA") == nullptr) {
-      // one 2D tensor map per (subdomain, field, box): halo box 36 x (IR2+2) at
-      // (c0-2, r0-1), centre box 32 x IR2; out-of-box elements are zero-filled
+    if (getenv("DDPMA_NO_TMA") == nullptr) {
+      // one tensor map per (subdomain, field, box).  2D: halo box 36 x (IR2+2)
+      // at (c0-2, r0-1), centre box 32 x IR2.  3D: halo box 36 x (TY+2) x
+      // (IZ3+2) at (c0-2, r0-1, z0-1), centre box 32 x TY x IZ3.  Out-of-box
+      // elements are zero-filled.
       typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1616,15 +1637,27 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
         bool ok = true;
         for (int l = 0; l < nl && ok; ++l) {
           const SubGeo& g = p->geo[l];
-          const cuuint64_t gdim[2] = {(cuuint64_t)g.n[1], (cuuint64_t)g.n[0]};
-          const cuuint64_t gstr[1] = {(cuuint64_t)g.pitch * 8};
-          const cuuint32_t estr[2] = {1, 1};
+          const bool d3 = p->dim == 3;
+          const cuuint32_t rank = d3 ? 3 : 2;
+          const cuuint64_t gdim[3] = {(cuuint64_t)(d3 ? g.n[2] : g.n[1]),
+                                      (cuuint64_t)(d3 ? g.n[1] : g.n[0]), (cuuint64_t)g.n[0]};
+          const cuuint64_t gstr[2] = {(cuuint64_t)g.pitch * 8,
+                                      (cuuint64_t)g.pitch * 8 * (cuuint64_t)g.n[1]};
+          const cuuint32_t estr[3] = {1, 1, 1};
           for (int f = 0; f < TF_N && ok; ++f) {
             for (int kind = 0; kind < 2; ++kind) {
-              const cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)(TX + 4) : (cuuint32_t)TX,
-                                         kind == 0 ? (cuuint32_t)(IR2 + 2) : (cuuint32_t)IR2};
+              cuuint32_t box[3];
+              if (!d3) {
+                box[0] = kind == 0 ? TX + 4 : TX;
+                box[1] = kind == 0 ? IR2 + 2 : IR2;
+                box[2] = 1;
+              } else {
+                box[0] = kind == 0 ? TX + 4 : TX;
+                box[1] = kind == 0 ? TY + 2 : TY;
+                box[2] = kind == 0 ? IZ3 + 2 : IZ3;
+              }
               CUresult r = enc(&maps[((size_t)l * TF_N + f) * 2 + kind], CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
-                               2, fields[f] + g.off, gdim, gstr, box, estr,
+                               rank, fields[f] + g.off, gdim, gstr, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
               if (r != CUDA_SUCCESS) ok = false;
@@ -1659,6 +1692,9 @@ ddpma_status reset_integrators(ddpma_plan* p) {
   memset(p->h_ctl, 0, sizeof(DevCtl) * nl);
   for (int l = 0; l < nl; ++l) p->h_ctl[l].interval = 25;   // _SIGMA_REFRESH
   CK(p, cudaMemcpyAsync(p->d_ctl, p->h_ctl, sizeof(DevCtl) * nl, cudaMemcpyHostToDevice, p->st));
+  // the sweep row counters start with the controllers (DevCtl::sbase = 0)
+  if (p->d_rowprog)
+    CK(p, cudaMemsetAsync(p->d_rowprog, 0, sizeof(unsigned long long) * std::max(1LL, p->total_rows), p->st));
   p->ctl_prev.assign(nl, DevCtl{});
   p->last_evals.assign(nl, 0);
   p->sub_evals.assign(nl, 0);
@@ -1988,6 +2024,34 @@ extern "C" ddpma_status ddpma_assemble_dev(ddpma_plan* p, double* psi, double* c
   a.nent = (int)ents.size();
   launch_assemble(a, nb, psi, coords, jac, p->st);
   if ((s = check_launch(p, "assemble")) != DDPMA_OK) return s;
+  return sync(p);
+}
+
+extern "C" ddpma_status ddpma_pack_owned(ddpma_plan* p, double* out_dev, int64_t* size) {
+  CK(p, cudaSetDevice(p->device));
+  const int nl = (int)p->local.size();
+  std::vector<long long> offs(nl);
+  long long tot = 0;
+  for (int l = 0; l < nl; ++l) {
+    const SubGeo& g = p->geo[l];
+    long long on = 1;
+    for (int q = 0; q < p->dim; ++q) on *= (long long)(g.ohi[q] - g.olo[q] + 1);
+    offs[l] = tot;
+    tot += on * (2 + p->dim);
+  }
+  if (size) *size = tot;
+  if (!out_dev) return DDPMA_OK;
+  int nb;
+  std::vector<Entry> ents = all_entries(p, &nb);
+  void *d, *d_offs;
+  ddpma_status s;
+  if ((s = stage_put(p, ents.data(), ents.size() * sizeof(Entry), &d)) != DDPMA_OK) return s;
+  if ((s = stage_put(p, offs.data(), offs.size() * sizeof(long long), &d_offs)) != DDPMA_OK) return s;
+  KArgs a = base_args(p);
+  a.ent = (Entry*)d;
+  a.nent = (int)ents.size();
+  launch_pack_owned(a, nb, out_dev, (const long long*)d_offs, p->st);
+  if ((s = check_launch(p, "pack_owned")) != DDPMA_OK) return s;
   return sync(p);
 }
 

@@ -61,6 +61,59 @@ def partition(dec: Decomposition, world: int) -> list[int]:
     return rank_of
 
 
+def partition_lpt(dec: Decomposition, world: int, weights) -> list[int]:
+    """rank_of[sub id] by greedy longest-processing-time: subdomains in order
+    of decreasing measured work (e.g. RHS evaluations x box nodes of the
+    previous window, Plan.sub_evals) go to the least-loaded rank (ties: the
+    lowest rank).  The reference's parallel_sweep balances nothing: its
+    thread pool takes subdomains in id order (schwarz.py:259-268)."""
+    w = np.asarray(weights, dtype=np.float64)
+    order = sorted(range(dec.nsub), key=lambda i: (-w[i], i))
+    load = np.zeros(world)
+    rank_of = [0] * dec.nsub
+    for i in order:
+        r = int(np.argmin(load))
+        rank_of[i] = r
+        load[r] += w[i]
+    return rank_of
+
+
+def makespan(weights, rank_of, world: int) -> tuple[float, float]:
+    """(max rank load, parallel efficiency sum/(world * max)) of a partition
+    under per-subdomain costs `weights` (a projection: no exchange cost, no
+    intra-window dynamics)."""
+    w = np.asarray(weights, dtype=np.float64)
+    load = np.zeros(world)
+    for i, r in enumerate(rank_of):
+        load[r] += w[i]
+    mx = float(load.max())
+    return mx, float(w.sum() / (world * mx)) if mx > 0 else 1.0
+
+
+def owned_sizes(dec: Decomposition, ids) -> list[int]:
+    """Packed length (ddpma_pack_owned layout) of each subdomain in `ids`."""
+    dim = dec.grid.dim
+    return [int(np.prod([hi - lo + 1 for lo, hi in dec.subdomains[i].owned])) * (2 + dim)
+            for i in ids]
+
+
+def unpack_owned(dec: Decomposition, ids, buf: torch.Tensor, psi: torch.Tensor,
+                 coords: torch.Tensor, jac: torch.Tensor) -> None:
+    """Scatter a ddpma_pack_owned buffer of subdomains `ids` (ascending) into
+    the global arrays (schwarz.py:271-282 assembly, on the device)."""
+    dim = dec.grid.dim
+    off = 0
+    for i in sorted(ids):
+        sub = dec.subdomains[i]
+        shape = tuple(hi - lo + 1 for lo, hi in sub.owned)
+        n = int(np.prod(shape))
+        gs = sub.owned_global_slices()
+        psi[gs] = buf[off:off + n].view(shape)
+        coords[gs] = buf[off + n:off + n * (1 + dim)].view(shape + (dim,))
+        jac[gs] = buf[off + n * (1 + dim):off + n * (2 + dim)].view(shape)
+        off += n * (2 + dim)
+
+
 class PlanEngine:
     """Adapter of the native plan to the engine interface."""
 
@@ -93,8 +146,14 @@ class PlanEngine:
     def assemble_into(self, psi: torch.Tensor, coords: torch.Tensor, jac: torch.Tensor):
         self.plan.assemble_dev(psi.data_ptr(), coords.data_ptr(), jac.data_ptr())
 
+    def pack_owned(self, out: torch.Tensor | None) -> int:
+        return self.plan.pack_owned(out.data_ptr() if out is not None and out.numel() else None)
+
     def sub_psi(self, sid):
         return self.plan.sub_psi(sid)
+
+    def sub_evals(self):
+        return self.plan.sub_evals()
 
     def counters(self):
         return self.plan.counters()
@@ -210,13 +269,135 @@ class ShardedSolver:
         return converged, stop
 
     def assemble(self):
-        """Owned blocks of every rank, reduced onto rank 0 (exact: disjoint)."""
+        """Owned blocks of every rank packed on the device (ddpma_pack_owned)
+        and gathered onto rank 0 with one all-gather over NCCL (SURVEY
+        §8(e)); rank 0 scatters them into the global psi / coords / jac.
+        Other ranks return None."""
+        n = self.engine.pack_owned(None)
+        buf = torch.empty(n, dtype=torch.float64, device=self.device)
+        self.engine.pack_owned(buf)
+        sizes = [sum(owned_sizes(self.dec, [i for i in range(self.dec.nsub)
+                                            if self.rank_of[i] == r])) for r in range(self.world)]
+        if self.world > 1:
+            mx = max(sizes)
+            send = torch.zeros(mx, dtype=torch.float64, device=self.device)
+            send[:n] = buf
+            if self.device.type == "cuda":
+                allb = torch.empty(self.world * mx, dtype=torch.float64, device=self.device)
+                dist.all_gather_into_tensor(allb, send, group=self.group)
+                parts = [allb[r * mx:r * mx + sizes[r]] for r in range(self.world)]
+            else:   # gloo (CPU test engines)
+                lst = [torch.empty(mx, dtype=torch.float64) for _ in range(self.world)]
+                dist.all_gather(lst, send, group=self.group)
+                parts = [lst[r][:sizes[r]] for r in range(self.world)]
+        else:
+            parts = [buf]
+        if self.rank != 0:
+            return None
         counts = tuple(self.grid.counts)
         psi = torch.zeros(counts, dtype=torch.float64, device=self.device)
         coords = torch.zeros(counts + (self.grid.dim,), dtype=torch.float64, device=self.device)
         jac = torch.zeros(counts, dtype=torch.float64, device=self.device)
-        self.engine.assemble_into(psi, coords, jac)
-        if self.world > 1:
-            for t in (psi, coords, jac):
-                dist.reduce(t, dst=0, group=self.group)
+        for r in range(self.world):
+            ids = [i for i in range(self.dec.nsub) if self.rank_of[i] == r]
+            unpack_owned(self.dec, ids, parts[r], psi, coords, jac)
         return psi, coords, jac
+
+
+class InProcessShards:
+    """`world` native plans on ONE device, each owning the subdomains with
+    rank_of[i] == r, stepped in lockstep with the per-window exchange done in
+    process (the all-reduce as a sum over plans, the all_to_all as a re-split
+    of the packed trace buffers, the owned blocks gathered as in
+    ShardedSolver.assemble).  It runs the exact native sharded code path of
+    a multi-GPU job (ddpma_density / _begin_window / _trace_counts /
+    _pack_traces / _apply_traces / _advance / _pack_owned) without needing
+    more than one GPU, and must be bitwise identical to a single-plan
+    solve.  The plans' kernels never wait on one another."""
+
+    def __init__(self, grid, dec, mon, config, rank_of, device=0, engines=None):
+        self.grid, self.dec, self.config = grid, dec, config
+        self.rank_of = list(rank_of)
+        self.world = max(self.rank_of) + 1
+        self.device = torch.device("cuda", device) if engines is None else engines[0].device
+        self.locals = [[i for i in range(dec.nsub) if self.rank_of[i] == r]
+                       for r in range(self.world)]
+        self.engines = engines if engines is not None else [
+            PlanEngine(grid, dec, mon, config, loc, device) for loc in self.locals]
+        self.splits = []
+        for r, e in enumerate(self.engines):
+            sc, rc = e.trace_counts(self.rank_of, self.world, r)
+            self.splits.append(([int(x) for x in sc], [int(x) for x in rc]))
+        self.send = [torch.zeros(sum(sc), dtype=torch.float64, device=self.device)
+                     for sc, _ in self.splits]
+        self.recv = [torch.zeros(sum(rc), dtype=torch.float64, device=self.device)
+                     for _, rc in self.splits]
+        self.history = []
+
+    def _stats(self):
+        tot = None
+        for e in self.engines:
+            t = np.stack(e.density())
+            tot = t if tot is None else tot + t   # one non-zero contributor per entry: exact
+        return tot
+
+    def set_state(self, initial=None):
+        for e in self.engines:
+            e.set_state(initial)
+        self.stats = self._stats()
+        self.history = []
+
+    def window(self):
+        z_part, raw_max = self.stats[0], self.stats[1]
+        z = 0.0
+        for v in z_part:                 # id order, as schwarz.py:182-186
+            z += float(v)
+        if not np.isfinite(z) or z <= 0.0:
+            raise InvalidMonitorError(f"transport quadrature of the mesh density is {z}")
+        rho_max = max(float(r) / z for r in raw_max)
+        for r, e in enumerate(self.engines):
+            e.begin_window(z, rho_max)
+            e.pack_traces(self.send[r])
+        # all_to_all_single: recv[r] gathers, in source-rank order, the
+        # segment of send[s] addressed to r
+        pieces = [list(torch.split(self.send[s], self.splits[s][0])) for s in range(self.world)]
+        for r in range(self.world):
+            if self.recv[r].numel():
+                torch.cat([pieces[s][r] for s in range(self.world)], out=self.recv[r])
+        for r, e in enumerate(self.engines):
+            e.apply_traces(self.recv[r])
+        errs = []
+        for e in self.engines:
+            try:
+                e.advance()
+            except (DdmeshError, ValueError, OverflowError) as err:
+                errs.append(err)
+        if errs:   # the lowest failing subdomain id wins (schwarz.py:262-268)
+            raise min(errs, key=lambda x: getattr(x, "subdomain", None) or 10 ** 9)
+        self.stats = self._stats()
+        res = self.stats[2]
+        stop = float(res.min() if self.config.stop_rule == "min" else res.max())
+        self.history.append((tuple(float(x) for x in res), stop, float(self.stats[3].min()),
+                             float(self.stats[4].max())))
+        return stop
+
+    def assemble(self):
+        counts = tuple(self.grid.counts)
+        psi = torch.zeros(counts, dtype=torch.float64, device=self.device)
+        coords = torch.zeros(counts + (self.grid.dim,), dtype=torch.float64, device=self.device)
+        jac = torch.zeros(counts, dtype=torch.float64, device=self.device)
+        for r, e in enumerate(self.engines):
+            n = e.pack_owned(None)
+            buf = torch.empty(n, dtype=torch.float64, device=self.device)
+            e.pack_owned(buf)
+            unpack_owned(self.dec, self.locals[r], buf, psi, coords, jac)
+        return psi, coords, jac
+
+    def sub_evals(self):
+        out = np.zeros(self.dec.nsub, dtype=np.int64)
+        for r, e in enumerate(self.engines):
+            out[self.locals[r]] = e.sub_evals()
+        return out
+
+    def node_updates(self):
+        return sum(e.counters()["node_updates"] for e in self.engines)

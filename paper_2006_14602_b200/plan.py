@@ -326,6 +326,14 @@ class Plan:
                                          _lib.dptr(fnew), C.byref(fl), C.byref(ef)))
         return d, fnew, bool(fl.value), bool(ef.value)
 
+    def pack_owned(self, out_ptr) -> int:
+        """ddpma_pack_owned: owned blocks of the local subdomains into the
+        device buffer at out_ptr (None: just the element count)."""
+        n = C.c_int64(0)
+        self.check(self.L.ddpma_pack_owned(self.h, C.c_void_p(out_ptr) if out_ptr else None,
+                                           C.byref(n)))
+        return int(n.value)
+
     def integrate_window(self, sub_id, y, rho, rho_max):
         """One window of the plan's integrator on box field ``y`` (returned
         as a new array) with a frozen nodal density (ddpma_integrate_window)."""

@@ -142,5 +142,21 @@ class OracleEngine:
             c[gs] = b.coords[ls]
             j[gs] = b.jac[ls]
 
+    def pack_owned(self, out):
+        """ddpma_pack_owned layout: per local subdomain (ascending id) its
+        owned block as [psi | coords (interleaved) | jac], C order."""
+        parts = []
+        for sid in sorted(self.boxes):
+            b = self.boxes[sid]
+            ls = b.sub.owned_l()
+            parts += [b.psi[ls].reshape(-1), b.coords[ls].reshape(-1), b.jac[ls].reshape(-1)]
+        flat = np.concatenate(parts) if parts else np.zeros(0)
+        if out is not None and out.numel():
+            out.copy_(torch.from_numpy(flat))
+        return flat.size
+
+    def sub_evals(self):
+        return np.zeros(len(self.local), dtype=np.int64)
+
     def counters(self):
         return {"node_updates": self.evals}

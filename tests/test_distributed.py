@@ -59,8 +59,9 @@ def _worker(rank, world, port, name, windows, rank_of, out):
                                rank_of=rank_of)
         solver.set_state(None)
         solver.run()
-        psi, coords, jac = solver.assemble()
+        out_ = solver.assemble()
         if rank == 0:
+            psi, coords, jac = out_
             np.savez(out, psi=psi.numpy(), coords=coords.numpy(), jac=jac.numpy(),
                      res=np.array([h[0] for h in solver.history]),
                      jmin=np.array([h[2] for h in solver.history]))
@@ -118,3 +119,61 @@ def test_alternating_refuses_sharding():
     with pytest.raises(P.DdmeshError):
         ShardedSolver(g, d, None, P.SolverConfig(transmission="alternating"), rank=0, world=2,
                       engine=object())
+
+
+def test_lpt_partition_and_makespan():
+    g = P.build_grid(2, ((0.0, 1.0),) * 2, (65, 65))
+    d = P.build_decomposition(g, (4, 4), 4)
+    from paper_2006_14602_b200.distributed import makespan, partition_lpt
+    rng = np.random.default_rng(1)
+    w = rng.uniform(1.0, 50.0, d.nsub)
+    for world in (2, 4, 8):
+        ro = partition_lpt(d, world, w)
+        mx, eff = makespan(w, ro, world)
+        # LPT bound: makespan <= (4/3 - 1/(3m)) * OPT, OPT >= max(mean load, max item)
+        opt_lb = max(w.sum() / world, w.max())
+        assert mx <= (4.0 / 3.0 - 1.0 / (3 * world)) * opt_lb + 1e-9
+        assert 0.0 < eff <= 1.0
+        assert sorted(set(ro)) == list(range(world))
+
+
+# ------------------------------------------------------------------- GPU ---
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,rank_of", [
+    ("C1", [0, 0, 1, 1]),
+    ("C1", [1, 0, 0, 1]),                      # interleaved: every face crosses ranks
+    ("C1", [0, 1, 2, 3]),
+    ("T3", [0, 1, 1, 0, 1, 0, 0, 1]),          # 3D, interleaved
+    ("T3", [0, 0, 1, 1, 2, 2, 3, 3]),
+])
+def test_native_sharded_plans_bitwise(name, rank_of):
+    """The native multi-GPU code path (PlanEngine: per-rank plans owning a
+    subset, ddpma_density / _begin_window / _trace_counts / _pack_traces /
+    _apply_traces / _advance / _pack_owned) with 2-4 plans on cuda:0 and the
+    exchange done in process: bitwise equal to the single-plan solve."""
+    from paper_2006_14602_b200.distributed import InProcessShards
+    if name == "C1":
+        g = P.build_grid(2, ((0.0, 1.0),) * 2, (65, 65))
+        d = P.build_decomposition(g, (2, 2), 4)
+        m = P.density_monitor(P.RingDensity(), g.extents)
+        windows = 12
+    else:
+        g = P.build_grid(3, ((0.0, 1.0),) * 3, (33, 33, 33))
+        d = P.build_decomposition(g, (2, 2, 2), 4)
+        m = P.density_monitor(P.ShellDensity(), g.extents)
+        windows = 6
+    cfg = P.SolverConfig(tol=1e-300, max_windows=windows, transmission="parallel")
+    ref = P.solve(g, d, m, cfg)
+    sh = InProcessShards(g, d, m, cfg, rank_of)
+    sh.set_state(None)
+    for _ in range(windows):
+        sh.window()
+    psi, coords, jac = (t.cpu().numpy() for t in sh.assemble())
+    assert np.array_equal(psi, ref.psi)
+    assert np.array_equal(coords, ref.mesh.coords)
+    assert np.array_equal(jac, ref.mesh.jac)
+    assert np.array_equal(np.array([h[0] for h in sh.history]),
+                          np.array([h.residuals for h in ref.history]))
+    assert np.array_equal(sh.sub_evals(), ref.stats["sub_rhs_evals"])
+    assert sh.node_updates() == ref.stats["node_updates"]

@@ -1,7 +1,15 @@
 """Summarise an ncu --set full capture of the window kernel into
-profiles/ncu_summary.json (read by bench.py for roofline.traffic)."""
-import csv, io, json, subprocess, sys
+profiles/ncu_summary.json (read by bench.py for roofline.traffic).
+
+    python tools/ncu_summary.py REPORT.ncu-rep PLAIN_WINDOW_COUNTS.log OUT.json [SOURCE_SHA]
+
+SOURCE_SHA is the sha256 of the kernel source (csrc/persist.cu) the capture
+ran; bench.py uses the traffic figure only while the source still matches."""
+import csv, hashlib, io, json, os, subprocess, sys
 rep, plain, out = sys.argv[1], sys.argv[2], sys.argv[3]
+src_sha = sys.argv[4] if len(sys.argv) > 4 else hashlib.sha256(open(os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+    "paper_2006_14602_b200", "csrc", "persist.cu"), "rb").read()).hexdigest()
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
@@ -31,6 +39,7 @@ summ = {
     "fp64_pipe_pct": get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
     "registers_per_thread": get("launch__registers_per_thread"),
     "note": "ncu replays serialize and run cold-cache; compare shares, not absolute time",
+    "persist_cu_sha256": src_sha,
 }
 json.dump(summ, open(out, "w"), indent=1)
 print(json.dumps(summ, indent=1))
