@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--until-tol", type=float, default=None,
                     help="time-to-converged mode: run windows until the stop rule meets TOL")
     ap.add_argument("--max-windows", type=int, default=5000)
+    ap.add_argument("--transmission", default="parallel", choices=["parallel", "alternating"],
+                    help="alternating = the id-ordered sweep (single GPU only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -83,8 +85,8 @@ def case(name, P):
     raise SystemExit(f"unknown config {name}")
 
 
-def solver_config(P, profile, windows):
-    kw = dict(tol=1e-300, max_windows=windows, transmission="parallel")
+def solver_config(P, profile, windows, transmission="parallel"):
+    kw = dict(tol=1e-300, max_windows=windows, transmission=transmission)
     if profile == "stable":
         kw.update(rtol=1e-6, atol=1e-9)
     return P.SolverConfig(**kw)
@@ -136,11 +138,15 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def kernel_name(dim):
-    if dim == 2 and os.environ.get("DDPMA_KERNEL", "D")[:1] != "P":
-        return ("k_windowD<pow2> persistent dataflow window kernel (RKC2 steps as level x item "
-                "task sweeps, TMA tile ring; 48 B/node-update at stage j>=4)")
-    return f"k_windowP<{dim},pow2> persistent window kernel (stage-by-stage actions)"
+def kernel_name(plan):
+    """The window kernel the plan launches (ddpma_window_kernel)."""
+    import paper_2006_14602_b200 as P
+    k = P._lib.lib().ddpma_window_kernel(plan.h).decode()
+    what = {"k_windowD": "persistent dataflow window kernel (RKC2 steps as level x item task "
+                         "sweeps, TMA tile ring)",
+            "k_windowP<2>": "persistent window kernel (stage-by-stage actions, 2D TMA tile ring)",
+            "k_windowP<3>": "persistent window kernel (stage-by-stage actions, 3D TMA tiles)"}
+    return f"{k}: {what.get(k, '')}; 48 B/node-update at stage j>=4"
 
 
 def peaks():
@@ -260,7 +266,7 @@ def run_gpu(args):
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     g, dec, mon = case(args.config, P)
     total_windows = args.warmup + args.steps
-    cfg = solver_config(P, args.profile, total_windows)
+    cfg = solver_config(P, args.profile, total_windows, args.transmission)
     engine = D.ShardedSolver(g, dec, mon, cfg, rank=rank, world=world,
                              device=local_rank) if world > 1 else None
     if engine is None:
@@ -328,7 +334,7 @@ def run_gpu(args):
                if traffic_per_node else None)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": kernel_name(g.dim),
+                "kernel": kernel_name(prof_plan),
                 "algo_bytes_per_launch": prof["bytes"][k] / max(1, int(prof["launches"][k])),
                 "avg_launch_ms": prof["ms"][k] / max(1, int(prof["launches"][k])),
                 "share_of_step": round(share, 4), "peak_source": peak_src}
@@ -347,7 +353,7 @@ def run_gpu(args):
         grids = np.meshgrid(*[a * a for a in ax], indexing="ij")
         psi_host[...] = 0.5 * np.sum(grids, axis=0)
         del grids
-        ecfg = solver_config(P, args.profile, args.steps)
+        ecfg = solver_config(P, args.profile, args.steps, args.transmission)
         t0 = time.perf_counter()
         res = P.solve(g, dec, mon, ecfg, initial=psi_host)
         et = time.perf_counter() - t0
@@ -381,7 +387,7 @@ def run_gpu(args):
                            "global_nodes": int(np.prod(g.counts)),
                            "subdomains": dec.nsub,
                            "box_nodes": int(sum(np.prod(s.shape()) for s in dec.subdomains)),
-                           "step": "one pseudo-time window (parallel transmission), "
+                           "step": f"one pseudo-time window ({args.transmission} transmission), "
                                    f"windows {args.warmup + 1}..{args.warmup + args.steps} "
                                    "of the solve from psi0",
                            "l2": "inputs larger than L2 (no flush needed)",

@@ -354,6 +354,9 @@ ddpma_status ddpma_profile(const ddpma_plan* plan, double* ms, double* bytes,
 
 /* The CUDA stream all plan work runs on (cudaStream_t as void*). */
 void* ddpma_stream(const ddpma_plan* plan);
+/* Name of the window kernel this plan's windows launch ("k_windowP<2>",
+ * "k_windowP<3>" or "k_windowD"): benchmark / profile labelling only. */
+const char* ddpma_window_kernel(const ddpma_plan* plan);
 
 /* ------------------------------------------------------ output formats ---
  * write_mesh_vtk (fileio.py:45-68): legacy-VTK structured grid, x fastest,

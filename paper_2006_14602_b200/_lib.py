@@ -107,6 +107,7 @@ SIGNATURES = {
     "ddpma_set_profiling": (C.c_int, [_P, C.c_int]),
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),
     "ddpma_stream": (C.c_void_p, [_P]),
+    "ddpma_window_kernel": (C.c_char_p, [_P]),
     "ddpma_monitor_mass": (C.c_int, [C.POINTER(Monitor), _I, C.c_int, _D, _D, _I]),
     "ddpma_write_mesh_vtk": (C.c_int, [C.c_char_p, C.c_int, _I, _D, _D, _D, C.c_char_p,
                                        C.c_char_p]),

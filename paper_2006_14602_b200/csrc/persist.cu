@@ -1536,7 +1536,10 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
 // those of k_windowP, so both kernels give bitwise identical results.
 // ============================================================================
 
-constexpr int NBD = 2;                // ring depth of k_windowD
+#ifndef DDPMA_NBD
+#define DDPMA_NBD 2
+#endif
+constexpr int NBD = DDPMA_NBD;        // ring depth of k_windowD
 constexpr int NWD = NT / 32;          // warps per CTA
 constexpr int M_EXIT = 99;            // ring-slot marker: no more work
 
@@ -1553,7 +1556,7 @@ struct SlotD {                        // the task whose tiles occupy stage[b]
 // that share an item row (same cell of a sweep) form a batch; the warp that
 // completes a batch's last item publishes the whole batch with one fence and
 // one atomic per counter (row progress, action completion).
-constexpr int NBB = 4;                // batch records (>= NBD + 2: see issue_next_d)
+constexpr int NBB = NBD + 2;          // batch records (>= NBD + 2: see fill_ring_d)
 struct BatchD {
   int sub, row, sweep, ntasks;
   int size, final_, pad0, pad1;
@@ -1700,8 +1703,10 @@ __device__ __forceinline__ void claim_d(const WinArgs& A, int chunk, int& got, i
 __device__ void fill_ring_d(const WinArgs& A, QueueD& q, SlotD* slot, BatchD* bat, Stage2* stage,
                             unsigned long long* full, unsigned long long* empty) {
   const int lane = threadIdx.x;
-  if (lane == 0)
+  if (lane == 0) {
     while (atomicCAS(&q.lock, 0, 1) != 0) __nanosleep(32);
+    __threadfence_block();   // acquire: the queue state left by the previous holder
+  }
   __syncwarp();
   unsigned backoff = 64;
   while (true) {
@@ -1849,7 +1854,10 @@ __device__ void fill_ring_d(const WinArgs& A, QueueD& q, SlotD* slot, BatchD* ba
     __syncwarp();
   }
   __syncwarp();
-  if (lane == 0) atomicExch(&q.lock, 0);
+  if (lane == 0) {
+    __threadfence_block();   // release: the queue state
+    atomicExch(&q.lock, 0);
+  }
 }
 
 // Fixed-order sum of the per-item partials of an action by one warp, in
@@ -2032,8 +2040,10 @@ __global__ void __launch_bounds__(NT, DDPMA_MINB2) k_windowD(const WinArgs A) {
     ++k;
     flush = __shfl_sync(0xffffffffu, flush, 0);
     if (flush) publish_batch_d<P2>(A, s_bat, bi, t, l, g, s_ctlw[warp]);
-    // the item is completed and published: this warp refills the ring
-    if (lane == 0) atomicAdd(&s_q.nfold, 1);
+    // the item is completed and published (by its last warp: one count per
+    // item, fill_ring_d compares it with the items issued); every warp then
+    // tries to refill the ring
+    if (last && lane == 0) atomicAdd(&s_q.nfold, 1);
     __syncwarp();
     fill_ring_d(A, s_q, s_slot, s_bat, stage, s_full, s_empty);
   }
@@ -2063,23 +2073,32 @@ __global__ void k_window_begin(const WinArgs A) {
 }  // namespace
 
 
-// The dataflow kernel k_windowD runs 2D windows (default); DDPMA_KERNEL=P
-// selects the stage-by-stage kernel k_windowP (A/B comparisons: bitwise
-// identical results).  3D windows run k_windowP<3>.
+// 2D windows run the stage-by-stage kernel k_windowP<2> or the dataflow kernel
+// k_windowD (bitwise identical results); DDPMA_KERNEL=P / D overrides the
+// built-in default below.  3D windows run k_windowP<3>.
+#ifndef DDPMA_DEFAULT_DATAFLOW
+#define DDPMA_DEFAULT_DATAFLOW 0
+#endif
 bool window_dataflow(int dim) {
-  static const bool p = getenv("DDPMA_KERNEL") && getenv("DDPMA_KERNEL")[0] == 'P';
-  return dim == 2 && !p;
+  static const int sel = [] {
+    const char* e = getenv("DDPMA_KERNEL");
+    if (e && e[0] == 'P') return 0;
+    if (e && e[0] == 'D') return 1;
+    return DDPMA_DEFAULT_DATAFLOW;
+  }();
+  return dim == 2 && sel != 0;
 }
 
-static int smem_bytes(int dim) {
-  return dim == 2 ? 2 * STAGE2_BYTES + 128 : 2 * (int)sizeof(Stage3) + 128;
+static int smem_bytes(int dim, bool dataflow) {
+  if (dim == 2) return (dataflow ? NBD : 2) * STAGE2_BYTES + 128;
+  return 2 * (int)sizeof(Stage3) + 128;
 }
 
 int window_blocks(int dim, int pow2) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int smem = smem_bytes(dim);
+  const int smem = smem_bytes(dim, window_dataflow(dim));
   const void* fn;
   if (dim == 2 && window_dataflow(2)) fn = pow2 ? (const void*)k_windowD<true> : (const void*)k_windowD<false>;
   else if (dim == 2) fn = pow2 ? (const void*)k_windowP<2, true> : (const void*)k_windowP<2, false>;
@@ -2102,7 +2121,8 @@ void launch_window(const WinArgs& a, int nb, void* stream) {
   if (a.P.dim == 2 && a.sweep) fn = a.P.pow2 ? (const void*)k_windowD<true> : (const void*)k_windowD<false>;
   else if (a.P.dim == 2) fn = a.P.pow2 ? (const void*)k_windowP<2, true> : (const void*)k_windowP<2, false>;
   else fn = a.P.pow2 ? (const void*)k_windowP<3, true> : (const void*)k_windowP<3, false>;
-  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem_bytes(a.P.dim), (cudaStream_t)stream);
+  cudaLaunchCooperativeKernel(fn, dim3(nb), blk, args, smem_bytes(a.P.dim, a.sweep != 0),
+                              (cudaStream_t)stream);
 }
 
 }  // namespace ddpma

@@ -119,6 +119,9 @@ struct ddpma_plan {
   int nsub = 0;
   std::vector<int> local;       // global ids, ascending
   std::vector<int> local_of;    // gid -> local index or -1
+  // alternating transmission: wavefront levels of the id-ordered sweep (local
+  // indices, ascending inside a level); only for plans owning every subdomain
+  std::vector<std::vector<int>> alt_levels;
   std::vector<SubGeo> geo;
   SubGeo* d_geo = nullptr;
   Prob P{};
@@ -1259,6 +1262,12 @@ extern "C" const char* ddpma_last_error(const ddpma_plan* p) {
 
 extern "C" void* ddpma_stream(const ddpma_plan* p) { return p ? (void*)p->st : nullptr; }
 
+extern "C" const char* ddpma_window_kernel(const ddpma_plan* p) {
+  if (!p) return "";
+  if (p->dim == 3) return "k_windowP<3>";
+  return (window_dataflow(2) && p->d_tmap != nullptr) ? "k_windowD" : "k_windowP<2>";
+}
+
 extern "C" void ddpma_plan_destroy(ddpma_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
@@ -1392,6 +1401,28 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
       return DDPMA_ERR_CONFIG;
     }
     p->local_of[p->local[l]] = l;
+  }
+  if ((int)p->local.size() == nsub) {
+    // level(l) = 1 + max level over the face donors / receivers of lower id
+    // (schwarz.py:216-233 visits ids in order; see ddpma_run).
+    // DDPMA_ALT_SERIAL=1 keeps one subdomain per launch (A/B comparisons).
+    const bool serial = getenv("DDPMA_ALT_SERIAL") != nullptr;
+    std::vector<int> level(nsub, 0);
+    for (int i = 0; i < nsub; ++i) {
+      int lev = 0;
+      if (serial) lev = i;
+      else
+        for (int m = 0; m < i; ++m) {
+          bool nb = false;
+          for (int k = 0; k < p->dim; ++k)
+            for (int side = 0; side < 2; ++side)
+              nb = nb || p->subs[i].donor[k][side] == m || p->subs[m].donor[k][side] == i;
+          if (nb && level[m] + 1 > lev) lev = level[m] + 1;
+        }
+      level[i] = lev;
+      if ((int)p->alt_levels.size() <= lev) p->alt_levels.resize(lev + 1);
+      p->alt_levels[lev].push_back(p->local_of[i]);
+    }
   }
   cudaError_t ce = cudaSetDevice(device);
   if (ce != cudaSuccess) {
@@ -1921,16 +1952,26 @@ extern "C" ddpma_status ddpma_run(ddpma_plan* p, int max_windows, double tol, do
       p->z = z;
       p->rho_max = rmax;
       set_guard(p, rmax);
-      for (int l = 0; l < n; ++l) {
-        std::vector<int> one{l};
-        if ((s = prologue(p, one, z)) != DDPMA_OK) return s;
+      // The sequential sweep only orders a subdomain after its face donors of
+      // lower id (it reads their advanced state) and before those of higher id
+      // (it reads their previous state): subdomains of one wavefront level
+      // (anti-diagonals of the lattice) are independent and share one window
+      // kernel launch.  Results are those of the id-ordered loop.
+      int cap = -1;   // a failure at id f: only ids < f can still change the report
+      for (const std::vector<int>& lev : p->alt_levels) {
+        std::vector<int> set;
+        for (int l : lev)
+          if (cap < 0 || p->local[l] < cap) set.push_back(l);
+        if (set.empty()) continue;
+        if ((s = prologue(p, set, z)) != DDPMA_OK) return s;
         std::vector<FaceJob> jobs;
         int nnodes = 0;
-        add_apply_jobs(p, l, 1, nullptr, jobs, nnodes);
+        for (int l : set) add_apply_jobs(p, l, 1, nullptr, jobs, nnodes);
         if ((s = run_faces(p, jobs, nnodes)) != DDPMA_OK) return s;
-        if ((s = advance_set(p, one)) != DDPMA_OK) return s;
-        if (p->fail.set) return report_failure(p);
+        if ((s = advance_set(p, set)) != DDPMA_OK) return s;
+        if (p->fail.set) cap = p->fail.gid;
       }
+      if (p->fail.set) return report_failure(p);
     }
     if ((s = mesh_pass(p, true)) != DDPMA_OK) return s;
     double stop = p->resid[0];

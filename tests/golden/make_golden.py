@@ -461,6 +461,52 @@ if __name__ == "__main__" and "prefix" in sys.argv[1:]:
     gen_prefix()
 
 
+# 1-ulp envelopes of the 3-window prefixes (test_c1_prefix_coords): the spread
+# of the reference itself when np.log is perturbed by one ulp, per variant.
+# Variants that raise the positivity flag inside the prefix (warm start,
+# max_stages=8) amplify 1-ulp differences above 1e-10 within three windows.
+PREFIX_ENV_RUNS = {
+    "C1_parallel": ("C1", dict(transmission="parallel"), None),
+    "C1_alternating": ("C1", dict(transmission="alternating"), None),
+    "C1_single": ("C1s", dict(), None),
+    "C1_warm": ("C1", dict(transmission="parallel"), "warm"),
+    "C1_cap8": ("C1", dict(transmission="alternating", max_stages=8), None),
+    "C1_slab4": ("C1slab", dict(transmission="parallel"), None),
+}
+
+
+def gen_prefix_envelopes():
+    out = {}
+    for tag, (kind, kw, init) in PREFIX_ENV_RUNS.items():
+        kw = dict(kw, max_windows=PREFIX_WINDOWS)
+        base = _oracle_run(kind, kw, init)
+        ec = ep = er = en = 0.0
+        for seed in (1, 2, 3, 4):
+            orig, noisy = _noisy_oracle(seed)
+            O.log_equi = noisy
+            try:
+                r = _oracle_run(kind, kw, init)
+            finally:
+                O.log_equi = orig
+            dp = r.psi - base.psi
+            ec = max(ec, float(np.abs(r.coords - base.coords).max()))
+            ep = max(ep, float(np.abs(dp - dp.mean()).max()))
+            rr, br = np.array(r.residuals), np.array(base.residuals)
+            er = max(er, float(np.max(np.abs(rr - br) / np.abs(br))))
+            en = max(en, abs(r.counter.node_updates - base.counter.node_updates)
+                     / base.counter.node_updates)
+        out[tag + "_coords"] = np.array(ec)
+        out[tag + "_psi_centered"] = np.array(ep)
+        out[tag + "_res_rel"] = np.array(er)
+        out[tag + "_nodes_rel"] = np.array(en)
+        print("prefix env", tag, ec, ep, er, en, flush=True)
+    np.savez(os.path.join(HERE, f"env_prefix{PREFIX_WINDOWS}_C1.npz"), **out)
+
+
+if __name__ == "__main__" and "prefix_envelopes" in sys.argv[1:]:
+    gen_prefix_envelopes()
+
+
 # ------------------------------------------------------ public API pins ----
 def gen_api():
     """The reference's public names (ddmesh.__all__) and host-helper outputs."""

@@ -149,7 +149,12 @@ def check_run(res, gold, tag=None, coord_tol=COORD_TOL):
         # prefix matches, or if the whole trajectory lies within the reference's
         # own spread under one-ulp perturbations (runs tangled from window 0).
         k = min(3, len(hr))
-        prefix_ok = rel_close(hr[:k], gold["residuals"][:k], 1e-9)
+        # prefix tolerance: 1e-9, or 4x the reference's own 1-ulp spread over
+        # that prefix where it is larger (warm start: flagged from window 0)
+        penv = golden("env_prefix3_C1.npz")
+        pkey = tag[:-4] if tag.endswith("_100") else tag
+        p_rtol = max(1e-9, 4.0 * float(penv[pkey + "_res_rel"])) if pkey + "_res_rel" in penv else 1e-9
+        prefix_ok = rel_close(hr[:k], gold["residuals"][:k], p_rtol)
         if "coords" in gold:
             dc = np.max(np.abs(res.mesh.coords - gold["coords"]))
         else:
@@ -419,10 +424,25 @@ def test_c1_prefix_coords(tag):
     dc = float(np.max(np.abs(res.mesh.coords - gold[tag + "_coords"])))
     dp = res.psi - gold[tag + "_psi"]
     dpc = float(np.max(np.abs(dp - dp.mean())))
-    print(f"[parity] {tag} prefix 3: max|dcoords|={dc:.3g} max|dpsi-const|={dpc:.3g}")
-    assert res.stats["node_updates"] == int(gold[tag + "_node_updates"])
-    assert rel_close(np.array([h.residuals for h in res.history]), gold[tag + "_residuals"], 1e-9)
-    assert dc <= COORD_TOL and dpc <= COORD_TOL
+    # The reference's own spread over this prefix when np.log is perturbed by
+    # one ulp (make_golden.py gen_prefix_envelopes): ~1e-11 for the cold
+    # starts, 6e-10 with max_stages=8, 1e-2 for the warm start (flagged from
+    # window 0).  Tolerance: 1e-10, or 4x that spread where it is larger.
+    env = golden("env_prefix3_C1.npz")
+    c_tol = max(COORD_TOL, 4.0 * float(env[tag + "_coords"]))
+    p_tol = max(COORD_TOL, 4.0 * float(env[tag + "_psi_centered"]))
+    r_tol = max(1e-9, 4.0 * float(env[tag + "_res_rel"]))
+    n_ref = int(gold[tag + "_node_updates"])
+    n_rel = abs(res.stats["node_updates"] - n_ref) / n_ref
+    hr = np.array([h.residuals for h in res.history])
+    gr = gold[tag + "_residuals"]
+    rr = float(np.max(np.abs(hr - gr) / np.abs(gr)))
+    print(f"[parity] {tag} prefix 3: max|dcoords|={dc:.3g} (tol {c_tol:.3g}) "
+          f"max|dpsi-const|={dpc:.3g} (tol {p_tol:.3g}) residual rel {rr:.3g} (tol {r_tol:.3g}) "
+          f"node-updates rel {n_rel:.3g}")
+    assert n_rel <= 4.0 * float(env[tag + "_nodes_rel"])   # exact where the reference's spread is 0
+    assert rr <= r_tol
+    assert dc <= c_tol and dpc <= p_tol
 
 
 def _window_case(name):
@@ -509,3 +529,26 @@ def test_rkc_step_baseline_boxes(name):
                 ef = float(np.max(np.abs(fnew - ofn))) / float(np.max(np.abs(ofn)))
                 print(f"[parity] rkc_step {name} box {sid} h={h} s={s}: d rel {ed:.3g}, f rel {ef:.3g}")
                 assert ed <= 1e-12 and ef <= 1e-12, (name, sid, h, s, ed, ef)
+
+
+@pytest.mark.parametrize("name,nwin", [("C2", 2), ("T3x3", 3)])
+def test_alternating_wavefront_equals_serial(name, nwin, monkeypatch):
+    """alternating_sweep (schwarz.py:216-233) visits subdomains in id order.
+    The device runs the independent subdomains of one wavefront level in one
+    window-kernel launch; DDPMA_ALT_SERIAL=1 is the literal one-by-one loop.
+    Both must give bitwise identical states and RHS-evaluation counts."""
+    if name == "C2":
+        og, g, d, mon, lay, raw = baseline("C2")
+    else:
+        g = P.build_grid(3, ((0.0, 1.0),) * 3, (49, 49, 49))
+        d = P.build_decomposition(g, (3, 3, 3), 3)
+        mon = P.density_monitor(P.ShellDensity(), g.extents)
+    cfg = P.SolverConfig(tol=1e-300, max_windows=nwin, transmission="alternating")
+    monkeypatch.delenv("DDPMA_ALT_SERIAL", raising=False)
+    a = P.solve(g, d, mon, cfg)
+    monkeypatch.setenv("DDPMA_ALT_SERIAL", "1")
+    b = P.solve(g, d, mon, cfg)
+    assert np.array_equal(a.stats["sub_rhs_evals"], b.stats["sub_rhs_evals"])
+    assert np.array_equal(a.psi, b.psi)
+    assert np.array_equal(a.mesh.coords, b.mesh.coords)
+    assert all(np.array_equal(x, y) for x, y in zip(a.sub_psi, b.sub_psi))
