@@ -10,7 +10,9 @@ OUT := paper_2006_14602_b200/libddpma.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # -fmad=false / -ffp-contract=off: no multiply-add contraction, so every
 # expression rounds exactly like the reference's numpy/Python arithmetic.
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v \
+# DDPMA_MINB2=3: the 2D window kernels at 80 registers, 3 CTAs per SM (measured on B200:
+# +11 % over 64 registers x 4 CTAs, +11 % over 128 registers x 2 CTAs; profiles/r2_variants.md)
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v -DDDPMA_MINB2=3 \
            -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude
 CXXFLAGS := -O2 -fPIC -std=c++17 -ffp-contract=off -Iinclude
 

@@ -30,7 +30,7 @@
 #include "crpow.cuh"
 
 #ifndef DDPMA_MINB2
-#define DDPMA_MINB2 4   // resident CTAs per SM of the 2D window kernel (register cap)
+#define DDPMA_MINB2 3   // resident CTAs per SM of the 2D window kernels (register cap 80)
 #endif
 
 namespace ddpma {
@@ -65,28 +65,6 @@ __shared__ double s_logtab[97][3];
 __device__ __forceinline__ double ldc(const double* p) { return __ldcg(p); }
 
 // ------------------------------------------------------------- accessors --
-
-template <int DIM, int YM>
-struct GAcc {   // Y from global memory (boundary nodes), coherent loads
-  const SubGeo* g;
-  const double* y;
-  const double* a;
-  double c;
-  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
-    const long long k = lin<DIM>(*g, i0, i1, i2);
-    const double yv = ldc(y + k);
-    if constexpr (YM == YM_PLAIN) {
-      return yv;
-    } else if constexpr (YM == YM_ADD) {
-      return yv + ldc(a + k);
-    } else if constexpr (YM == YM_SCALED) {
-      return yv + c * ldc(a + k);
-    } else {
-      const int par = (i0 + i1 + (DIM == 3 ? i2 : 0)) & 1;
-      return yv + (par ? -c : c);
-    }
-  }
-};
 
 struct Act {      // the action of the claimed item (broadcast through smem)
   int mode, j, s, yi, fi, vin, vout, sub;
@@ -591,47 +569,51 @@ __device__ __forceinline__ double yat(const Stage2& st, int p, double c, int par
   }
 }
 
-// Y for the generic (box-face) formulas: from the smem tile when the point
-// lies inside it (always, except for 1-3 row/column slivers at a box end),
-// else from global memory.
-template <int YM, int YMG = YM>
-struct TileAcc2 {
-  const Stage2* st;
-  int r0, c0;
-  GAcc<2, YMG> g;
-  __device__ __forceinline__ double operator()(int i0, int i1, int) const {
-    const int rr = i0 - r0 + 1, cc = i1 - c0 + 2;
-    if (rr >= 0 && rr < TH2 && cc >= 0 && cc < TW2) {
-      const int p = rr * TW2 + cc;
-      if constexpr (YM == YM_PLAIN) {
-        return st->ys[p];
-      } else if constexpr (YM == YM_ADD) {
-        return st->ys[p] + st->as[p];
-      } else if constexpr (YM == YM_SCALED) {
-        return st->ys[p] + g.c * st->as[p];
-      } else {
-        return st->ys[p] + (((i0 + i1) & 1) ? -g.c : g.c);
-      }
-    }
-    return g(i0, i1, 0);
+// Determinant at a box-face node that is NOT Dirichlet.  Inside the window
+// kernels every non-physical box face is an interface (Dirichlet) face, so such
+// a node lies on physical faces only: per axis the second difference is the
+// interior formula or the Neumann-ghost formula of _second_diff
+// (pma.py:87-115, d2ax), the cross term is zero on a physical face
+// (pma.py:118-130, cross) -- every Y it needs is within one node, i.e. inside
+// the staged tile.  Same expressions, same order as hdet<2>'s generic branch
+// (bitwise identical); the one-sided 4-point formulas of hdet<> can never be
+// reached here and are not instantiated (they were most of the kernel's code).
+template <bool P2, int YM>
+__device__ __forceinline__ double hdet2_face(const Prob& P, const SubGeo& g, int i0, int i1,
+                                             const Stage2& st, int p, double c, int par) {
+  const int n0 = g.n[0], n1 = g.n[1];
+  const double yc = yat<YM>(st, p, c, par);
+  double h00, h11, h01 = 0.0;
+  if (i0 == 0)
+    h00 = dv<P2>(2.0 * ((yat<YM>(st, p + TW2, c, par ^ 1) - yc) - g.halo[0]), P.ax[0].hh, P.ax[0].ihh);
+  else if (i0 == n0 - 1)
+    h00 = dv<P2>(2.0 * ((yat<YM>(st, p - TW2, c, par ^ 1) - yc) + g.hahi[0]), P.ax[0].hh, P.ax[0].ihh);
+  else
+    h00 = dv<P2>((yat<YM>(st, p + TW2, c, par ^ 1) - 2.0 * yc) + yat<YM>(st, p - TW2, c, par ^ 1),
+                 P.ax[0].hh, P.ax[0].ihh);
+  if (i1 == 0)
+    h11 = dv<P2>(2.0 * ((yat<YM>(st, p + 1, c, par ^ 1) - yc) - g.halo[1]), P.ax[1].hh, P.ax[1].ihh);
+  else if (i1 == n1 - 1)
+    h11 = dv<P2>(2.0 * ((yat<YM>(st, p - 1, c, par ^ 1) - yc) + g.hahi[1]), P.ax[1].hh, P.ax[1].ihh);
+  else
+    h11 = dv<P2>((yat<YM>(st, p + 1, c, par ^ 1) - 2.0 * yc) + yat<YM>(st, p - 1, c, par ^ 1),
+                 P.ax[1].hh, P.ax[1].ihh);
+  if (!(i0 == 0 || i0 == n0 - 1 || i1 == 0 || i1 == n1 - 1)) {
+    const double gp = dv<P2>(yat<YM>(st, p + TW2 + 1, c, par) - yat<YM>(st, p + TW2 - 1, c, par),
+                             P.ax[1].twoh, P.ax[1].itwoh);
+    const double gm = dv<P2>(yat<YM>(st, p - TW2 + 1, c, par) - yat<YM>(st, p - TW2 - 1, c, par),
+                             P.ax[1].twoh, P.ax[1].itwoh);
+    h01 = dv<P2>(gp - gm, P.ax[0].twoh, P.ax[0].itwoh);
   }
-};
+  return h00 * h11 - h01 * h01;
+}
 
 template <bool P2, int MODE, int YM>
 __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
                                          int r0, const Stage2& st, Acc& acc, double* psum_item) {
   constexpr int R = IR2 / TY;
-  // how Y is formed from global memory (outside the tile) for this mode
-  constexpr int YMG = MODE == M_STAGE2 ? YM_SCALED
-                      : (MODE == M_STAGE3 || MODE == M_STAGEN) ? YM_ADD : YM;
   const int n0 = g.n[0], n1 = g.n[1];
   const int i1 = c0 + threadIdx.x;
-  const double* yb = A.F.y[t.yi];
-  const double* ap = nullptr;
-  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
-  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
-  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
-  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
   if constexpr (MODE == M_NORM) {
     double ps = 0.0;
 #pragma unroll
@@ -687,8 +669,9 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
           if (dirichlet<2>(g, i0, i1, 0)) {
             dirm |= 1u << q;
           } else {
-            det[q] = hdet<2, P2>(A.P, g, i0, i1, 0,
-                                 TileAcc2<YM, YMG>{&st, r0, c0, GAcc<2, YMG>{&g, yb, ap, t.c}});
+            const int lr = threadIdx.y + q * TY;
+            det[q] = hdet2_face<P2, YM>(A.P, g, i0, i1, st, (lr + 1) * TW2 + threadIdx.x + 2, t.c,
+                                        (i0 + i1) & 1);
           }
         }
       }
@@ -749,15 +732,6 @@ __device__ __forceinline__ void compute2(const WinArgs& A, const SubGeo& g, cons
   }
 }
 
-// Face-node determinant (generic one-sided formulas, hdet<2>).
-template <bool P2, int YM>
-__device__ __forceinline__ double hdet_face(const WinArgs& A, const SubGeo& g, const Act& t, int i0,
-                                         int i1, int r0, int c0, const Stage2& st,
-                                         const double* yb, const double* ap) {
-  return hdet<2, P2>(A.P, g, i0, i1, 0,
-                     TileAcc2<YM, YM>{&st, r0, c0, GAcc<2, YM>{&g, yb, ap, t.c}});
-}
-
 // Fused RHS + epilogue of one 2D item for the modes without partial sums
 // (F0, EULER, STAGE2/3/N, FINAL).  Thread (tx, ty) owns the two consecutive
 // rows 2ty and 2ty+1 of column tx, so the 3x4 Y neighbourhood is loaded once
@@ -800,11 +774,6 @@ __device__ __forceinline__ void compute2_int(const WinArgs& A, const SubGeo& g, 
   }
   unsigned valid = 3u, dirm = 0u;
   if constexpr (EDGE) {
-    const double* yb = A.F.y[t.yi];
-    const double* ap = nullptr;
-    if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
-    if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
-    if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
     const int i1 = c0 + tx;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -813,7 +782,7 @@ __device__ __forceinline__ void compute2_int(const WinArgs& A, const SubGeo& g, 
         valid &= ~(1u << q);
       } else if (i0 == 0 || i0 == n0 - 1 || i1 == 0 || i1 == n1 - 1) {
         if (dirichlet<2>(g, i0, i1, 0)) dirm |= 1u << q;
-        else det[q] = hdet_face<P2, YM>(A, g, t, i0, i1, r0, c0, st, yb, ap);
+        else det[q] = hdet2_face<P2, YM>(A.P, g, i0, i1, st, p + q * TW2, t.c, par ^ q);
       }
     }
   }
@@ -1165,29 +1134,6 @@ __device__ __forceinline__ void issue3_tma(const WinArgs& A, int l, const Act& t
   }
 }
 
-template <int YM, int YMG = YM>
-struct TileAcc3 {
-  const Stage3* st;
-  int z0, r0, c0;
-  GAcc<3, YMG> g;
-  __device__ __forceinline__ double operator()(int i0, int i1, int i2) const {
-    const int zz = i0 - z0 + 1, rr = i1 - r0 + 1, cc = i2 - c0 + 2;
-    if (zz >= 0 && zz < TD3 && rr >= 0 && rr < TH3 && cc >= 0 && cc < TW2) {
-      const int p = (zz * TH3 + rr) * TW2 + cc;
-      if constexpr (YM == YM_PLAIN) {
-        return st->ys[p];
-      } else if constexpr (YM == YM_ADD) {
-        return st->ys[p] + st->as[p];
-      } else if constexpr (YM == YM_SCALED) {
-        return st->ys[p] + g.c * st->as[p];
-      } else {
-        return st->ys[p] + (((i0 + i1 + i2) & 1) ? -g.c : g.c);
-      }
-    }
-    return g(i0, i1, i2);
-  }
-};
-
 template <int YM>
 __device__ __forceinline__ double yat3(const Stage3& st, int p, double c, int par) {
   if constexpr (YM == YM_PLAIN) {
@@ -1201,20 +1147,46 @@ __device__ __forceinline__ double yat3(const Stage3& st, int p, double c, int pa
   }
 }
 
+// 3D twin of hdet2_face: the determinant at a non-Dirichlet box-face node
+// (physical faces only), every Y from the staged tile; hdet<3>'s generic
+// branch restricted to the formulas reachable here, same expressions and
+// order (bitwise identical).
+template <bool P2, int YM>
+__device__ __forceinline__ double hdet3_face(const Prob& P, const SubGeo& g, int i0, int i1,
+                                             int i2, const Stage3& st, int p, double c, int par) {
+  const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+  const double yc = yat3<YM>(st, p, c, par);
+  auto Y1 = [&](int off) { return yat3<YM>(st, p + off, c, par ^ 1); };   // one axis step
+  auto Y2 = [&](int off) { return yat3<YM>(st, p + off, c, par); };       // two axis steps
+  auto d2 = [&](int ax, int i, int n, int off) {
+    if (i == 0) return dv<P2>(2.0 * ((Y1(off) - yc) - g.halo[ax]), P.ax[ax].hh, P.ax[ax].ihh);
+    if (i == n - 1) return dv<P2>(2.0 * ((Y1(-off) - yc) + g.hahi[ax]), P.ax[ax].hh, P.ax[ax].ihh);
+    return dv<P2>((Y1(off) - 2.0 * yc) + Y1(-off), P.ax[ax].hh, P.ax[ax].ihh);
+  };
+  const double h00 = d2(0, i0, n0, SZ3);
+  const double h11 = d2(1, i1, n1, SY3);
+  const double h22 = d2(2, i2, n2, 1);
+  const bool on0 = i0 == 0 || i0 == n0 - 1, on1 = i1 == 0 || i1 == n1 - 1,
+             on2 = i2 == 0 || i2 == n2 - 1;
+  auto cr = [&](bool onface, int k, int l, int offk, int offl) {   // d/dk of d/dl
+    if (onface) return 0.0;
+    const double gp = dv<P2>(Y2(offk + offl) - Y2(offk - offl), P.ax[l].twoh, P.ax[l].itwoh);
+    const double gm = dv<P2>(Y2(-offk + offl) - Y2(-offk - offl), P.ax[l].twoh, P.ax[l].itwoh);
+    return dv<P2>(gp - gm, P.ax[k].twoh, P.ax[k].itwoh);
+  };
+  const double h01 = cr(on0 || on1, 0, 1, SZ3, SY3);
+  const double h02 = cr(on0 || on2, 0, 2, SZ3, 1);
+  const double h12 = cr(on1 || on2, 1, 2, SY3, 1);
+  return (h00 * (h11 * h22 - h12 * h12) - h01 * (h01 * h22 - h12 * h02)) +
+         h02 * (h01 * h12 - h11 * h02);
+}
+
 template <bool P2, int MODE, int YM>
 __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, const Act& t, int c0,
                                          int r0, int z0, const Stage3& st, Acc& acc,
                                          double* psum_item) {
-  constexpr int YMG = MODE == M_STAGE2 ? YM_SCALED
-                      : (MODE == M_STAGE3 || MODE == M_STAGEN) ? YM_ADD : YM;
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int i1 = r0 + threadIdx.y, i2 = c0 + threadIdx.x;
-  const double* yb = A.F.y[t.yi];
-  const double* ap = nullptr;
-  if constexpr (MODE == M_STAGE2) ap = A.F.f[t.fi];
-  if constexpr (MODE == M_STAGE3 || MODE == M_STAGEN) ap = A.F.d[(t.j - 1) % 3];
-  if constexpr (MODE == M_FINAL) ap = A.F.d[t.s % 3];
-  if constexpr (MODE == M_POWER) ap = A.F.d[t.vin];
   const long long plane = (long long)n1 * g.pitch;
   double ps = 0.0;
 #pragma unroll
@@ -1263,11 +1235,13 @@ __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, cons
         const double h12 = dv<P2>(gp - gm, A.P.ax[1].twoh, A.P.ax[1].itwoh);
         det = (h00 * (h11 * h22 - h12 * h12) - h01 * (h01 * h22 - h12 * h02)) +
               h02 * (h01 * h12 - h11 * h02);
-      } else {
-        det = hdet<3, P2>(A.P, g, i0, i1, i2,
-                          TileAcc3<YM, YMG>{&st, z0, r0, c0, GAcc<3, YMG>{&g, yb, ap, t.c}});
       }
+      // box-face nodes: interface (Dirichlet) faces need no determinant (F = 0,
+      // never flagged); physical faces take the Neumann-ghost formulas
       const bool dir = !interior && dirichlet<3>(g, i0, i1, i2);
+      if (!interior)
+        det = dir ? 0.0
+                  : hdet3_face<P2, YM>(A.P, g, i0, i1, i2, st, p, t.c, (i0 + i1 + i2) & 1);
       const double F = dir ? 0.0 : logequi(st.cm[pc], det, A.P.guard, A.P.floor, A.P.rguard, s_logtab);
       acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
       if constexpr (MODE == M_F0) {
@@ -1394,7 +1368,7 @@ __device__ void dispatch_chunk3(const WinArgs& A, const SubGeo& g, const Act& t,
 }
 
 template <int DIM, bool P2>
-__global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(const WinArgs A) {
+__global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(const __grid_constant__ WinArgs A) {
   using Stage = typename std::conditional<DIM == 2, Stage2, Stage3>::type;
   extern __shared__ __align__(128) unsigned char dsm[];
   Stage* stage = reinterpret_cast<Stage*>(
@@ -1416,7 +1390,13 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
   __shared__ Act s_act;
   __shared__ DevCtl s_ctl;
   __shared__ int s_sub, s_it0, s_nit, s_exit, s_last;
+  __shared__ unsigned s_bits;
+  __shared__ unsigned long long s_emax;
   const int tid = threadIdx.y * TX + threadIdx.x;
+  if (tid == 0) {
+    s_bits = 0u;
+    s_emax = 0ull;
+  }
   unsigned backoff = 32;
   while (true) {
     if (threadIdx.y == 0) {
@@ -1465,17 +1445,33 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
     if constexpr (DIM == 2)
       dispatch_chunk2<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_mbar, phases);
     else dispatch_chunk3<P2>(A, g, t, it0, nit, stage, acc, sh_sum, s_mbar, phases);
-    const int any = __syncthreads_or(acc.flag);
-    const int anynf = __syncthreads_or(acc.nonfin);
-    unsigned long long emax = 0ull;
-    if (t.mode == M_FINAL)
-      emax = block_max_u64((unsigned long long)__double_as_longlong(acc.ratio), sh_max);
-    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
+    // chunk completion: flags / error ratio folded per warp (shuffles), then
+    // through shared accumulators -- one CTA barrier, not one per quantity
+    {
+      const unsigned wb = __reduce_or_sync(0xffffffffu, (acc.flag ? 1u : 0u) | (acc.nonfin ? 4u : 0u));
+      unsigned long long em = (unsigned long long)__double_as_longlong(acc.ratio);
+      if (t.mode == M_FINAL) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long o = __shfl_down_sync(0xffffffffu, em, off);
+          em = o > em ? o : em;
+        }
+      }
+      if (threadIdx.x == 0) {
+        if (wb) atomicOr(&s_bits, wb);
+        if (t.mode == M_FINAL && em) atomicMax(&s_emax, em);
+      }
+    }
+    __syncthreads();
     if (tid == 0) {
       DevCtl* gc = A.ctl + l;
+      const unsigned wb = s_bits;
+      const unsigned long long emax = s_emax;
+      s_bits = 0u;
+      s_emax = 0ull;
       unsigned bits = 0;
-      if (any) bits |= t.mode == M_FINAL ? 2u : 1u;
-      if (anynf) bits |= 4u;
+      if (wb & 1u) bits |= t.mode == M_FINAL ? 2u : 1u;
+      if (wb & 4u) bits |= 4u;
       if (bits) atomicOr(&gc->acc_flags, bits);
       if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
       __threadfence();
@@ -1492,6 +1488,7 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
     if (s_last) {
       __threadfence();
       double sum = 0.0;
+      const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
       if (sums) {
         double v = 0.0;
         for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
@@ -1499,7 +1496,8 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
       }
       if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
     }
-    __syncthreads();
+    // no barrier here: the other warps wait for warp 0's next claim at the top
+    // of the loop; nothing they still read is written before that barrier
   }
 }
 
@@ -1703,6 +1701,20 @@ __device__ __forceinline__ void claim_d(const WinArgs& A, int chunk, int& got, i
 __device__ void fill_ring_d(const WinArgs& A, QueueD& q, SlotD* slot, BatchD* bat, Stage2* stage,
                             unsigned long long* full, unsigned long long* empty) {
   const int lane = threadIdx.x;
+  {
+    // Lock-free early out: the next slot is still being read by some warp.
+    // That warp calls fill_ring_d after it arrives on the slot's empty
+    // barrier, so nothing is lost by returning.  (q.issued can only grow
+    // while we look; a slot issued meanwhile reads as free: we then take the
+    // lock and look again.)
+    int go = 1;
+    if (lane == 0) {
+      const int n = *(volatile int*)&q.issued;
+      const unsigned u = (unsigned)(n / NBD);
+      if (u >= 1 && !mbar_test(&empty[n % NBD], (u - 1) & 1u)) go = 0;
+    }
+    if (!__shfl_sync(0xffffffffu, go, 0)) return;
+  }
   if (lane == 0) {
     while (atomicCAS(&q.lock, 0, 1) != 0) __nanosleep(32);
     __threadfence_block();   // acquire: the queue state left by the previous holder
@@ -1946,7 +1958,7 @@ __device__ __noinline__ void publish_batch_d(const WinArgs& A, BatchD* s_bat, in
 }
 
 template <bool P2>
-__global__ void __launch_bounds__(NT, DDPMA_MINB2) k_windowD(const WinArgs A) {
+__global__ void __launch_bounds__(NT, DDPMA_MINB2) k_windowD(const __grid_constant__ WinArgs A) {
   extern __shared__ __align__(128) unsigned char dsm[];
   Stage2* stage = reinterpret_cast<Stage2*>(
       dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));

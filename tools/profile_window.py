@@ -9,8 +9,9 @@ from paper_2006_14602_b200.plan import Plan
 import bench
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 W = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+DTAU = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-3
 g, d, m = bench.case(name, P)
-plan = Plan.for_grid(g, d.subdomains, m, P.SolverConfig(tol=1e-300, max_windows=W + 1, transmission="parallel"))
+plan = Plan.for_grid(g, d.subdomains, m, P.SolverConfig(tol=1e-300, max_windows=W + 1, transmission="parallel", dtau=DTAU))
 plan.set_state(None)
 prev = plan.counters()
 for w in range(W + 1):
