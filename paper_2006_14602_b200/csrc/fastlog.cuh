@@ -41,22 +41,55 @@ __host__ __device__ __forceinline__ double fastlog_t(double x, const double (*ta
 #else
 #define DDPMA_FMA(a, b, c) std::fma((a), (b), (c))
 #endif
-  long long bits;
-  memcpy(&bits, &x, 8);
-  int e = (int)(bits >> 52) - 1023;
-  if (!(x >= 0x1p-1022 && x < INFINITY)) {   // one test for the common (positive normal) case
+  // Decomposition on the high word only (32-bit integer ops; on the device the
+  // 64-bit versions of these were ~20 instructions per call).
+  unsigned xhi, xlo;
+#ifdef __CUDA_ARCH__
+  xhi = (unsigned)__double2hiint(x);
+  xlo = (unsigned)__double2loint(x);
+#else
+  {
+    unsigned long long b;
+    memcpy(&b, &x, 8);
+    xhi = (unsigned)(b >> 32);
+    xlo = (unsigned)b;
+  }
+#endif
+  int e;
+  if (xhi - 0x00100000u < 0x7fe00000u) {   // positive normal: one unsigned compare
+    e = (int)(xhi >> 20) - 1023;
+  } else {
     if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
     if (x == INFINITY) return x;
     const double xs = x * 0x1p54;   // subnormal: scale into the normal range
-    memcpy(&bits, &xs, 8);
-    e = (int)(bits >> 52) - 1023 - 54;
+#ifdef __CUDA_ARCH__
+    xhi = (unsigned)__double2hiint(xs);
+    xlo = (unsigned)__double2loint(xs);
+#else
+    unsigned long long b;
+    memcpy(&b, &xs, 8);
+    xhi = (unsigned)(b >> 32);
+    xlo = (unsigned)b;
+#endif
+    e = (int)(xhi >> 20) - 1023 - 54;
   }
-  const long long hb = (bits >> 51) & 1;   // m0 >= 1.5 -> m = m0/2
+  const unsigned hb = (xhi >> 19) & 1u;   // m0 >= 1.5 -> m = m0/2
   e += (int)hb;
-  const long long mb = (bits & 0x000FFFFFFFFFFFFFLL) | ((1023LL - hb) << 52);
+  const unsigned mh = (xhi & 0x000FFFFFu) | ((1023u - hb) << 20);
   double m;
-  memcpy(&m, &mb, 8);
-  const int k = (int)(m * 128.0 + 0.5);
+#ifdef __CUDA_ARCH__
+  m = __hiloint2double((int)mh, (int)xlo);
+#else
+  {
+    const unsigned long long b = ((unsigned long long)mh << 32) | xlo;
+    memcpy(&m, &b, 8);
+  }
+#endif
+  // k = (int)(m * 128.0 + 0.5), from the mantissa bits: m in [1, 1.5) ->
+  // 128 + round-half-up(f * 128), m in [0.75, 1) -> 64 + round-half-up(f * 64)
+  // (f = fraction; bits below the high word cannot move the floor)
+  const unsigned f20 = xhi & 0x000FFFFFu;
+  const int k = hb ? 64 + (int)((f20 + (1u << 13)) >> 14) : 128 + (int)((f20 + (1u << 12)) >> 13);
   const double* t = tab[k - 96];
   const double pm = m * t[0];                   // m*inv = pm + plo exactly
   const double plo = DDPMA_FMA(m, t[0], -pm);

@@ -1293,14 +1293,24 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     z0 = (rest / g.items_y) * IZ3;
   };
   // TMA (cp.async.bulk.tensor.3d) with mbarrier completion when the plan has
-  // 3D tensor maps; cp.async otherwise.  Stage (i+1)&1 is refilled only after
-  // the CTA barrier that ends item i-1.
+  // 3D tensor maps; cp.async otherwise.  TMA pipeline as in chunk2: mbar[b] =
+  // "buffer b full", mbar[2+b] = "buffer b consumed" (one arrival per warp);
+  // the issuing thread waits for the previous use of a buffer to be consumed,
+  // so no CTA barrier ends an item.
   const bool tma = A.tmap != nullptr;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   int c0, r0, z0, nc0 = 0, nr0 = 0, nz0 = 0;
   origin(it0, c0, r0, z0);
+  auto issue = [&](int b, int x, int y, int z) {
+    if ((phases >> (4 + b)) & 1u) {
+      mbar_wait(&mbar[2 + b], (phases >> (2 + b)) & 1u);
+      phases ^= 1u << (2 + b);
+    }
+    phases |= 1u << (4 + b);
+    issue3_tma<MODE, YM>(A, t.sub, t, x, y, z, stage[b], &mbar[b]);
+  };
   if (tma) {
-    if (lead) issue3_tma<MODE, YM>(A, t.sub, t, c0, r0, z0, stage[0], &mbar[0]);
+    if (lead) issue(0, c0, r0, z0);
   } else {
     issue3<MODE, YM>(A, g, t, c0, r0, z0, stage[0]);
   }
@@ -1309,7 +1319,7 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     if (i + 1 < nit) {
       origin(it0 + i + 1, nc0, nr0, nz0);
       if (tma) {
-        if (lead) issue3_tma<MODE, YM>(A, t.sub, t, nc0, nr0, nz0, stage[sb ^ 1], &mbar[sb ^ 1]);
+        if (lead) issue(sb ^ 1, nc0, nr0, nz0);
       } else {
         issue3<MODE, YM>(A, g, t, nc0, nr0, nz0, stage[sb ^ 1]);
         cpa_wait<1>();
@@ -1323,9 +1333,14 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     } else {
       __syncthreads();
     }
-    constexpr bool COMBINED = MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN;
+#ifndef DDPMA_3D_COMBINED
+#define DDPMA_3D_COMBINED 1
+#endif
+    // COMBINED: Y = y + a (stage increments) formed once per tile element in
+    // shared memory instead of once per stencil read
+    constexpr bool COMBINED = DDPMA_3D_COMBINED && (MODE == M_STAGE2 || MODE == M_STAGE3 || MODE == M_STAGEN);
     if constexpr (COMBINED) {
-      Stage3& sg = stage[i & 1];
+      Stage3& sg = stage[sb];
       const int tid = threadIdx.y * TX + threadIdx.x;
       for (int e = tid; e < TD3 * TH3 * TW2; e += NT) {
         if constexpr (YM == YM_ADD) sg.ys[e] = sg.ys[e] + sg.as[e];
@@ -1334,12 +1349,16 @@ __device__ void chunk3(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
       __syncthreads();
     }
     double ps = 0.0;
-    compute3<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, c0, r0, z0, stage[i & 1], acc, &ps);
+    compute3<P2, MODE, COMBINED ? YM_PLAIN : YM>(A, g, t, c0, r0, z0, stage[sb], acc, &ps);
+    if (tma) {
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&mbar[2 + sb]);   // this warp is done with buffer sb
+    }
     if constexpr (SUMS) {
       const double s = block_sum(ps, sh_sum);
       if (threadIdx.x == 0 && threadIdx.y == 0) __stcg(A.part + A.poff[t.sub] + it0 + i, s);
     } else {
-      __syncthreads();
+      if (!tma) __syncthreads();   // the stage buffer is refilled by the next iteration's issue
     }
     c0 = nc0;
     r0 = nr0;
