@@ -439,6 +439,10 @@ struct Stage2 {
   double cd[IR2 * TX];
 };
 constexpr int STAGE2_BYTES = (int)sizeof(Stage2);
+#ifndef DDPMA_RING2
+#define DDPMA_RING2 2
+#endif
+constexpr int RD2 = DDPMA_RING2;   // depth of k_windowP<2>'s TMA tile ring
 
 __device__ __forceinline__ void cpa16(double* sdst, const double* gsrc, int bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -945,6 +949,23 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
   // box geometry in registers (the geo table is immutable during the kernel)
   const int n0 = __ldg(&g.n[0]), n1 = __ldg(&g.n[1]), items_x = __ldg(&g.items_x);
   const long long pitch = __ldg(&g.pitch), goff = __ldg(&g.off);
+  const bool tma = A.tmap != nullptr;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  // TMA pipeline, RD2 stages deep: mbar[b] = "buffer b full" (1 arrival + tx
+  // bytes), mbar[RD2+b] = "buffer b consumed" (one arrival per warp).  phases:
+  // bits [0,RD2) full parity, [RD2,2RD2) consumed parity, [2RD2,3RD2) buffer
+  // used before.  The issuing thread waits for the previous use of a buffer
+  // to be consumed by every warp, so warps never meet at a CTA barrier
+  // between items; item i+RD2-1 is in flight while item i is computed.
+  auto issue = [&](int b, int item) {
+    if ((phases >> (2 * RD2 + b)) & 1u) {
+      mbar_wait(&mbar[RD2 + b], (phases >> (RD2 + b)) & 1u);
+      phases ^= 1u << (RD2 + b);
+    }
+    phases |= 1u << (2 * RD2 + b);
+    const int cy = item / items_x, cx = item - cy * items_x;
+    issue2_tma<MODE, YM>(A, t.sub, t, cx * TX, cy * IR2, stage[b], &mbar[b]);
+  };
   // item -> (column, row) tile origin, decoded once per chunk then stepped
   int ix = it0 % items_x, iy = it0 / items_x;
   int nx = ix + 1, ny = iy;
@@ -952,30 +973,16 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     nx = 0;
     ++ny;
   }
-  const bool tma = A.tmap != nullptr;
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-  // TMA pipeline: mbar[b] = "buffer b full" (1 arrival + tx bytes), mbar[2+b]
-  // = "buffer b consumed" (one arrival per warp).  phases: bits 0-1 full
-  // parity, 2-3 consumed parity, 4-5 buffer used before.  The issuing thread
-  // waits for the previous use of a buffer to be consumed by every warp, so
-  // warps never meet at a CTA barrier between items.
-  auto issue = [&](int b, int cx, int cy) {
-    if ((phases >> (4 + b)) & 1u) {
-      mbar_wait(&mbar[2 + b], (phases >> (2 + b)) & 1u);
-      phases ^= 1u << (2 + b);
-    }
-    phases |= 1u << (4 + b);
-    issue2_tma<MODE, YM>(A, t.sub, t, cx * TX, cy * IR2, stage[b], &mbar[b]);
-  };
   if (tma) {
-    if (lead) issue(0, ix, iy);
+    if (lead)
+      for (int k = 0; k < RD2 - 1 && k < nit; ++k) issue(k, it0 + k);
   } else {
     issue2<MODE, YM>(A, g, t, ix * TX, iy * IR2, stage[0]);
   }
   for (int i = 0; i < nit; ++i) {
-    const int s = i & 1;
+    const int s = tma ? i % RD2 : (i & 1);
     if (tma) {
-      if (i + 1 < nit && lead) issue(s ^ 1, nx, ny);
+      if (i + RD2 - 1 < nit && lead) issue((i + RD2 - 1) % RD2, it0 + i + RD2 - 1);
       mbar_wait(&mbar[s], (phases >> s) & 1u);
       phases ^= 1u << s;
     } else {
@@ -1005,7 +1012,7 @@ __device__ void chunk2(const WinArgs& A, const SubGeo& g, const Act& t, int it0,
     }
     if (tma) {
       __syncwarp();
-      if (threadIdx.x == 0) mbar_arrive(&mbar[2 + s]);   // this warp is done with buffer s
+      if (threadIdx.x == 0) mbar_arrive(&mbar[RD2 + s]);   // this warp is done with buffer s
     }
     if constexpr (SUMS) {
       const double s = block_sum(ps, sh_sum);   // per-item partial: deterministic
@@ -1392,13 +1399,14 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
   extern __shared__ __align__(128) unsigned char dsm[];
   Stage* stage = reinterpret_cast<Stage*>(
       dsm + ((128 - ((unsigned)__cvta_generic_to_shared(dsm) & 127u)) & 127u));
-  __shared__ __align__(8) unsigned long long s_mbar[4];
+  constexpr int RD = DIM == 2 ? RD2 : 2;   // ring depth: full barriers [0,RD), consumed [RD,2RD)
+  __shared__ __align__(8) unsigned long long s_mbar[2 * RD];
   unsigned phases = 0u;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
-    mbar_init(&s_mbar[0]);
-    mbar_init(&s_mbar[1]);
-    mbar_init_n(&s_mbar[2], NT / 32);
-    mbar_init_n(&s_mbar[3], NT / 32);
+    for (int b = 0; b < RD; ++b) {
+      mbar_init(&s_mbar[b]);
+      mbar_init_n(&s_mbar[RD + b], NT / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int i = threadIdx.y * TX + threadIdx.x; i < 97 * 3; i += NT)
@@ -2121,7 +2129,7 @@ bool window_dataflow(int dim) {
 }
 
 static int smem_bytes(int dim, bool dataflow) {
-  if (dim == 2) return (dataflow ? NBD : 2) * STAGE2_BYTES + 128;
+  if (dim == 2) return (dataflow ? NBD : RD2) * STAGE2_BYTES + 128;
   return 2 * (int)sizeof(Stage3) + 128;
 }
 
