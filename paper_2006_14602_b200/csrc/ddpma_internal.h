@@ -220,6 +220,8 @@ struct WinArgs {
   unsigned long long* probe;   // debug: [cap][4] = publish, first claim, last done, decided
   int probe_sub, probe_cap;
   int chunk_bulk;            // items per claim while >= tail_n subdomains are active
+  const int* chunk_q;        // per priority position q (parallel to act[]): items per claim of
+                             // that subdomain in the bulk phase (<= chunk_bulk), or nullptr
   int chunk_tail, tail_n;    // items per claim below that (the tail's critical path)
   const void* tmap;          // 2D: CUtensorMap[nlocal][8 fields][2 boxes] (TMA tile loads), or null
   int sweep;                 // 1: RKC2 steps run as M_SWEEP dataflow actions (k_windowD)

@@ -844,10 +844,14 @@ __device__ __forceinline__ void claim(const WinArgs& A, int chunk, int& got, int
     const int q = base + lane;
     int l = -1;
     bool claimable = false;
+    int mychunk = chunk;
     if (q < A.nact) {
       l = A.act[q];
       const unsigned long long w = *(volatile unsigned long long*)&A.ctl[l].word;
       claimable = w_cursor(w) < w_ntasks(w);
+      // bulk phase: the subdomain's own chunk size (small for the subdomains
+      // whose sequential chain of actions would otherwise outlast the window)
+      if (A.chunk_q != nullptr && chunk == A.chunk_bulk) mychunk = __ldg(A.chunk_q + q);
     }
     unsigned mask = __ballot_sync(0xffffffffu, claimable);
     while (mask != 0u && got < 0) {
@@ -855,6 +859,7 @@ __device__ __forceinline__ void claim(const WinArgs& A, int chunk, int& got, int
       mask &= mask - 1u;
       int it = -1, n = 0;
       if (lane == src) {
+        const int chunk = mychunk;
         const unsigned long long w2 = atomicAdd(&A.ctl[l].word, (unsigned long long)chunk);
         const unsigned u = w_cursor(w2);
         const unsigned ni = w_ntasks(w2);

@@ -187,7 +187,7 @@ struct ddpma_plan {
   int* d_coef_off = nullptr;
   double* d_part_items = nullptr;
   long long* d_poff = nullptr;
-  int* d_act = nullptr;
+  int* d_act = nullptr;       // [0, nl): priority order; [nl, 2nl): per-position chunk sizes
   int* h_act = nullptr;
   unsigned int* d_ndone = nullptr;
   TraceRec* d_trace = nullptr;
@@ -195,6 +195,7 @@ struct ddpma_plan {
   int trace_cap = 0;
   int win_blocks = 0;
   int chunk_bulk = 8, chunk_tail = 2, tail_n = 16;   // window scheduler knobs (parsed once)
+  bool chunk_adapt = true;   // per-subdomain bulk chunk sizes from the last window's tallies
   unsigned long long* d_probe = nullptr;             // DDPMA_PROBE timestamps (debug)
   unsigned long long* d_rowprog = nullptr;           // k_windowD per-row task counters
   long long total_rows = 0;
@@ -843,7 +844,30 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
     return p->last_evals[x] * p->geo[x].nodes > p->last_evals[y] * p->geo[y].nodes;
   });
   for (size_t q = 0; q < order.size(); ++q) p->h_act[q] = order[q];
-  CK(p, cudaMemcpyAsync(p->d_act, p->h_act, sizeof(int) * act.size(), cudaMemcpyHostToDevice, p->st));
+  // Per-subdomain chunk size.  A subdomain's actions are a sequential chain: an
+  // action claimed in chunks of c items takes ~(c + o) item-times (o ~ 2: claim,
+  // first tile, completion, controller), so a subdomain with n actions cannot
+  // finish before n (c + o).  The window as a whole needs ~T = (all items) /
+  // (CTAs) item-times.  Subdomains whose chain at the bulk chunk size would
+  // reach 0.6 T (from the previous window's action counts) get smaller chunks,
+  // so the heaviest subdomains finish early instead of leaving a serial tail.
+  {
+    int* hq = p->h_act + nl;
+    double items_tot = 0.0;
+    for (int l : act) items_tot += (double)p->last_evals[l] * (double)p->geo[l].nitems;
+    const double T = items_tot / (double)std::max(1, p->win_blocks);
+    for (size_t q = 0; q < order.size(); ++q) {
+      const long long n = p->last_evals[order[q]];
+      int c = p->chunk_bulk;
+      if (p->chunk_adapt && n > 0 && T > 0.0) {
+        const double cmax = 0.6 * T / (double)n - 2.0;
+        c = cmax >= (double)p->chunk_bulk ? p->chunk_bulk : (cmax < 2.0 ? 2 : (int)cmax);
+      }
+      hq[q] = c;
+    }
+    for (size_t q = order.size(); q < (size_t)nl; ++q) hq[q] = p->chunk_bulk;
+  }
+  CK(p, cudaMemcpyAsync(p->d_act, p->h_act, sizeof(int) * 2 * nl, cudaMemcpyHostToDevice, p->st));
   CK(p, cudaMemsetAsync(p->d_ndone, 0, sizeof(unsigned int) * 2, p->st));
   WinArgs A{};
   A.P = p->P;
@@ -865,6 +889,7 @@ ddpma_status advance_set(ddpma_plan* p, const std::vector<int>& act) {
   A.trace_n = p->d_trace_n;
   A.trace_cap = p->trace_cap;
   A.chunk_bulk = p->chunk_bulk;
+  A.chunk_q = p->d_act + nl;
   A.chunk_tail = p->chunk_tail;
   A.tail_n = p->tail_n;
   A.tmap = p->d_tmap;
@@ -1380,6 +1405,7 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
   p->chunk_bulk = knob[0];
   p->chunk_tail = knob[1];
   p->tail_n = knob[2];
+  if (const char* e = getenv("DDPMA_CHUNK_ADAPT")) p->chunk_adapt = e[0] != '0';   // A/B knob
   p->device = device;
   p->grid = *grid;
   p->cfg = *cfg;
@@ -1630,8 +1656,8 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     if ((ce = cudaMalloc((void**)&p->d_poff, sizeof(long long) * nl)) != cudaSuccess) return fail(ce, "poff");
     if ((ce = cudaMemcpy(p->d_poff, poff.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice)) != cudaSuccess)
       return fail(ce, "poff copy");
-    if ((ce = cudaMalloc((void**)&p->d_act, sizeof(int) * nl)) != cudaSuccess) return fail(ce, "act");
-    if ((ce = cudaMallocHost((void**)&p->h_act, sizeof(int) * nl)) != cudaSuccess) return fail(ce, "act host");
+    if ((ce = cudaMalloc((void**)&p->d_act, sizeof(int) * 2 * nl)) != cudaSuccess) return fail(ce, "act");
+    if ((ce = cudaMallocHost((void**)&p->h_act, sizeof(int) * 2 * nl)) != cudaSuccess) return fail(ce, "act host");
     if ((ce = cudaMalloc((void**)&p->d_ndone, sizeof(unsigned int) * 2)) != cudaSuccess) return fail(ce, "ndone");
     p->d_trace_n = p->d_ndone + 1;
     if (g_trace) {
