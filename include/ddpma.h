@@ -170,6 +170,15 @@ ddpma_status ddpma_build_decomposition(int dim, const int* counts,
                                        const int* layout, int overlap,
                                        ddpma_subdomain* out, int cap, int* nsub);
 
+/* Wavefront levels of alternating_sweep (schwarz.py:216-233).  The sweep
+ * visits subdomains in id order; subdomain i only has to follow its face
+ * donors / receivers of lower id, so level[i] = 1 + max level over those (0
+ * without any): subdomains of one level are mutually independent and the
+ * device advances them in one window-kernel launch, levels in ascending order
+ * (bitwise the id-ordered result).  Pure host code.  Returns the number of
+ * levels; level[] has nsub entries. */
+int ddpma_alternating_levels(int dim, const ddpma_subdomain* subs, int nsub, int* level);
+
 /* RKC2 recurrence coefficients (integrate.py:77-106) for s stages:
  * out arrays have s+1 entries (index j as in the reference). */
 ddpma_status ddpma_rkc_coeffs(int s, double* w0, double* w1, double* mu1t,

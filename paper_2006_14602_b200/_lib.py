@@ -106,6 +106,7 @@ SIGNATURES = {
     "ddpma_sub_evals": (C.c_int, [_P, _I64, C.c_int]),
     "ddpma_set_profiling": (C.c_int, [_P, C.c_int]),
     "ddpma_profile": (C.c_int, [_P, _D, _D, _I64, _I64, C.c_int]),
+    "ddpma_alternating_levels": (C.c_int, [C.c_int, C.POINTER(Subdomain), C.c_int, _I]),
     "ddpma_stream": (C.c_void_p, [_P]),
     "ddpma_window_kernel": (C.c_char_p, [_P]),
     "ddpma_monitor_mass": (C.c_int, [C.POINTER(Monitor), _I, C.c_int, _D, _D, _I]),

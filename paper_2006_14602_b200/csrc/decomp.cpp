@@ -222,6 +222,23 @@ extern "C" ddpma_status ddpma_build_decomposition(int dim, const int* counts,
 
 // integrate.py:77-106 — damped RKC2 coefficients (host scalar arithmetic in
 // the reference's evaluation order; compiled with -ffp-contract=off).
+extern "C" int ddpma_alternating_levels(int dim, const ddpma_subdomain* subs, int nsub, int* level) {
+  int nlev = 0;
+  for (int i = 0; i < nsub; ++i) {
+    int lev = 0;
+    for (int m = 0; m < i; ++m) {
+      bool nb = false;
+      for (int k = 0; k < dim; ++k)
+        for (int side = 0; side < 2; ++side)
+          nb = nb || subs[i].donor[k][side] == m || subs[m].donor[k][side] == i;
+      if (nb && level[m] + 1 > lev) lev = level[m] + 1;
+    }
+    level[i] = lev;
+    if (lev + 1 > nlev) nlev = lev + 1;
+  }
+  return nlev;
+}
+
 extern "C" ddpma_status ddpma_rkc_coeffs(int s, double* w0o, double* w1o, double* mu1to,
                                          double* mu, double* nu, double* mut, double* gt) {
   if (s < 2) {

@@ -1434,20 +1434,13 @@ extern "C" ddpma_status ddpma_plan_create(const ddpma_grid* grid, const ddpma_su
     // DDPMA_ALT_SERIAL=1 keeps one subdomain per launch (A/B comparisons).
     const bool serial = getenv("DDPMA_ALT_SERIAL") != nullptr;
     std::vector<int> level(nsub, 0);
+    if (serial)
+      for (int i = 0; i < nsub; ++i) level[i] = i;
+    else
+      ddpma_alternating_levels(p->dim, p->subs.data(), nsub, level.data());
     for (int i = 0; i < nsub; ++i) {
-      int lev = 0;
-      if (serial) lev = i;
-      else
-        for (int m = 0; m < i; ++m) {
-          bool nb = false;
-          for (int k = 0; k < p->dim; ++k)
-            for (int side = 0; side < 2; ++side)
-              nb = nb || p->subs[i].donor[k][side] == m || p->subs[m].donor[k][side] == i;
-          if (nb && level[m] + 1 > lev) lev = level[m] + 1;
-        }
-      level[i] = lev;
-      if ((int)p->alt_levels.size() <= lev) p->alt_levels.resize(lev + 1);
-      p->alt_levels[lev].push_back(p->local_of[i]);
+      if ((int)p->alt_levels.size() <= level[i]) p->alt_levels.resize(level[i] + 1);
+      p->alt_levels[level[i]].push_back(p->local_of[i]);
     }
   }
   cudaError_t ce = cudaSetDevice(device);

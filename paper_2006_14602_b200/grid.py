@@ -134,6 +134,19 @@ def to_c(sub: Subdomain, dim: int) -> _lib.Subdomain:
     return out
 
 
+def alternating_levels(dec: "Decomposition") -> list[int]:
+    """Wavefront level of every subdomain under alternating transmission
+    (native host code, ``ddpma_alternating_levels``): the id-ordered sweep of
+    ``ddmesh/schwarz.py:216-233`` only orders a subdomain after its face
+    neighbours of lower id, so equal-level subdomains are independent and the
+    device advances them in one launch."""
+    dim = len(dec.subdomains[0].pos)
+    arr = (_lib.Subdomain * dec.nsub)(*[to_c(s, dim) for s in dec.subdomains])
+    lev = (C.c_int * dec.nsub)()
+    _lib.lib().ddpma_alternating_levels(dim, arr, dec.nsub, lev)
+    return list(lev)
+
+
 def build_decomposition(grid: CompGrid, layout, overlap: int = 3) -> Decomposition:
     """Overlapping slab/block decomposition (grid.py:176-237), computed by the
     native host layer; bit-exact boxes, ownership, faces and donor ids."""

@@ -86,6 +86,29 @@ def test_native_decomposition_property_sweep(dim):
                    (b.id, b.pos, b.box, b.faces, b.neighbors, b.owned)
 
 
+@pytest.mark.parametrize("counts,layout,ov", [((65, 65), (2, 2), 4), ((513, 513), (4, 4), 8),
+                                              ((257, 257), (8, 8), 4), ((65, 65), (4, 1), 3),
+                                              ((65, 65, 65), (4, 4, 4), 3), ((33, 33, 33), (2, 3, 2), 2)])
+def test_alternating_wavefront_levels(counts, layout, ov):
+    """ddpma_alternating_levels: the id-ordered alternating sweep
+    (schwarz.py:216-233) as wavefront levels.  Level = 1 + max over face
+    neighbours of lower id; neighbours never share a level; on a lattice the
+    levels are the anti-diagonals (sum of lattice positions)."""
+    from paper_2006_14602_b200.grid import alternating_levels
+    dim = len(counts)
+    g = P.build_grid(dim, [(0.0, 1.0)] * dim, counts)
+    d = P.build_decomposition(g, layout, ov)
+    lev = alternating_levels(d)
+    assert len(lev) == d.nsub
+    for s in d.subdomains:
+        nbs = [n for n in s.neighbors.values() if n is not None and n >= 0]
+        lower = [lev[n] for n in nbs if n < s.id]
+        assert lev[s.id] == (1 + max(lower) if lower else 0)
+        assert all(lev[n] != lev[s.id] for n in nbs)
+        assert lev[s.id] == sum(s.pos)
+    assert max(lev) + 1 == sum(n - 1 for n in layout) + 1
+
+
 def test_rkc_coefficients_bitwise():
     for s in (2, 3, 4, 9, 23, 64, 257, 512):
         got = P.rkc_coeffs(s)
