@@ -1495,7 +1495,13 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
       }
     }
     __syncthreads();
-    if (tid == 0) {
+    // Completion bookkeeping (global atomics, ~1.5 us of round trips) runs on
+    // warp 1 while warp 0 already claims the next chunk: the two latencies
+    // overlap instead of adding up at every chunk boundary.  The actions with
+    // a partial sum (norm / power iteration: rare) need every thread for the
+    // fixed-order reduction and keep the serial form.
+    const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
+    auto complete = [&]() -> int {   // one thread: publish this chunk's results
       DevCtl* gc = A.ctl + l;
       const unsigned wb = s_bits;
       const unsigned long long emax = s_emax;
@@ -1508,25 +1514,35 @@ __global__ void __launch_bounds__(NT, DIM == 2 ? DDPMA_MINB2 : 3) k_windowP(cons
       if (t.mode == M_FINAL) atomicMax(&gc->acc_emax, emax);
       __threadfence();
       const unsigned d = atomicAdd(&gc->done, (unsigned)nit);
-      s_last = d + (unsigned)nit == (unsigned)g.nitems;
-      if (s_last && A.probe && l == A.probe_sub) {
+      const int last = d + (unsigned)nit == (unsigned)g.nitems;
+      if (last && A.probe && l == A.probe_sub) {
         unsigned long long now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         const unsigned long long sq = w_seq(*(volatile unsigned long long*)&gc->word);
         A.probe[(sq % (unsigned long long)A.probe_cap) * 4 + 2] = now;
       }
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      double sum = 0.0;
-      const bool sums = t.mode == M_POWER || t.mode == M_POWER_SEED || t.mode == M_NORM;
-      if (sums) {
+      return last;
+    };
+    if (!sums) {
+      if (threadIdx.y == 1) {
+        int last = 0;
+        if (threadIdx.x == 0) last = complete();
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+          decide(A, l, g, 0.0, s_ctl);
+        }
+      }
+    } else {
+      if (tid == 0) s_last = complete();
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
         double v = 0.0;
         for (int i = tid; i < g.nitems; i += NT) v += __ldcg(A.part + A.poff[l] + i);
-        sum = block_sum(v, sh_sum);
+        const double sum = block_sum(v, sh_sum);
+        if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
       }
-      if (threadIdx.y == 0) decide(A, l, g, sum, s_ctl);
     }
     // no barrier here: the other warps wait for warp 0's next claim at the top
     // of the loop; nothing they still read is written before that barrier
