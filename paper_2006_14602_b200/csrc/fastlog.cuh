@@ -33,46 +33,15 @@ __constant__ double kLogPolyD[6] = DDPMA_LOGPOLY;
 #endif
 static const double kLogPolyH[6] = DDPMA_LOGPOLY;
 
-// `tab` = the {inv_k, T_hi, T_lo} table (kLogTabD in global memory, or a
-// shared-memory copy of it in the window kernel).
-__host__ __device__ __forceinline__ double fastlog_t(double x, const double (*tab)[3]) {
+// The branch-free part of fastlog_t: x = 2^e * (mantissa given by xhi/xlo), a
+// positive normal number (or a subnormal already scaled by the caller).
+__host__ __device__ __forceinline__ double fastlog_core(unsigned xhi, unsigned xlo, int e,
+                                                        const double (*tab)[3]) {
 #ifdef __CUDA_ARCH__
 #define DDPMA_FMA(a, b, c) __fma_rn((a), (b), (c))
 #else
 #define DDPMA_FMA(a, b, c) std::fma((a), (b), (c))
 #endif
-  // Decomposition on the high word only (32-bit integer ops; on the device the
-  // 64-bit versions of these were ~20 instructions per call).
-  unsigned xhi, xlo;
-#ifdef __CUDA_ARCH__
-  xhi = (unsigned)__double2hiint(x);
-  xlo = (unsigned)__double2loint(x);
-#else
-  {
-    unsigned long long b;
-    memcpy(&b, &x, 8);
-    xhi = (unsigned)(b >> 32);
-    xlo = (unsigned)b;
-  }
-#endif
-  int e;
-  if (xhi - 0x00100000u < 0x7fe00000u) {   // positive normal: one unsigned compare
-    e = (int)(xhi >> 20) - 1023;
-  } else {
-    if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
-    if (x == INFINITY) return x;
-    const double xs = x * 0x1p54;   // subnormal: scale into the normal range
-#ifdef __CUDA_ARCH__
-    xhi = (unsigned)__double2hiint(xs);
-    xlo = (unsigned)__double2loint(xs);
-#else
-    unsigned long long b;
-    memcpy(&b, &xs, 8);
-    xhi = (unsigned)(b >> 32);
-    xlo = (unsigned)b;
-#endif
-    e = (int)(xhi >> 20) - 1023 - 54;
-  }
   const unsigned hb = (xhi >> 19) & 1u;   // m0 >= 1.5 -> m = m0/2
   e += (int)hb;
   const unsigned mh = (xhi & 0x000FFFFFu) | ((1023u - hb) << 20);
@@ -117,6 +86,55 @@ __host__ __device__ __forceinline__ double fastlog_t(double x, const double (*ta
   const double bv = a - s;
   const double e2 = (s - (a - bv)) + (r - bv);
   return a + (e2 + lo);
+#undef DDPMA_FMA
+}
+
+// x is a positive normal double: the test fastlog_t makes first.
+__host__ __device__ __forceinline__ bool fastlog_normal(unsigned xhi) {
+  return xhi - 0x00100000u < 0x7fe00000u;
+}
+
+// `tab` = the {inv_k, T_hi, T_lo} table (kLogTabD in global memory, or a
+// shared-memory copy of it in the window kernel).
+__host__ __device__ __forceinline__ double fastlog_t(double x, const double (*tab)[3]) {
+#ifdef __CUDA_ARCH__
+#define DDPMA_FMA(a, b, c) __fma_rn((a), (b), (c))
+#else
+#define DDPMA_FMA(a, b, c) std::fma((a), (b), (c))
+#endif
+  // Decomposition on the high word only (32-bit integer ops; on the device the
+  // 64-bit versions of these were ~20 instructions per call).
+  unsigned xhi, xlo;
+#ifdef __CUDA_ARCH__
+  xhi = (unsigned)__double2hiint(x);
+  xlo = (unsigned)__double2loint(x);
+#else
+  {
+    unsigned long long b;
+    memcpy(&b, &x, 8);
+    xhi = (unsigned)(b >> 32);
+    xlo = (unsigned)b;
+  }
+#endif
+  int e;
+  if (xhi - 0x00100000u < 0x7fe00000u) {   // positive normal: one unsigned compare
+    e = (int)(xhi >> 20) - 1023;
+  } else {
+    if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;   // log(+-0) = -inf, log(<0 | NaN) = NaN
+    if (x == INFINITY) return x;
+    const double xs = x * 0x1p54;   // subnormal: scale into the normal range
+#ifdef __CUDA_ARCH__
+    xhi = (unsigned)__double2hiint(xs);
+    xlo = (unsigned)__double2loint(xs);
+#else
+    unsigned long long b;
+    memcpy(&b, &xs, 8);
+    xhi = (unsigned)(b >> 32);
+    xlo = (unsigned)b;
+#endif
+    e = (int)(xhi >> 20) - 1023 - 54;
+  }
+  return fastlog_core(xhi, xlo, e, tab);
 #undef DDPMA_FMA
 }
 

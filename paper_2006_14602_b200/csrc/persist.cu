@@ -790,11 +790,16 @@ __device__ __forceinline__ void compute2_int(const WinArgs& A, const SubGeo& g, 
       }
     }
   }
+  {
+    // nodes past the box (EDGE) carry zero-filled tiles: no F needed either
+    const unsigned skip = dirm | (~valid & 3u);
+    const double mrv[2] = {st.cm[lr * TX + tx], st.cm[(lr + 1) * TX + tx]};
+    const double g_ = A.P.guard;
+    logequi_pair(mrv, det, skip, g_, A.P.floor, A.P.rguard, g_ >= 0x1p-900 && g_ < 0x1p900, s_logtab, F);
+  }
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int pc = (lr + q) * TX + tx;
     const bool dir = (dirm >> q) & 1u;
-    F[q] = dir ? 0.0 : logequi(st.cm[pc], det[q], A.P.guard, A.P.floor, A.P.rguard, s_logtab);
     acc.flag |= ((valid >> q) & 1u) && !dir && det[q] <= A.P.floor ? 1u : 0u;
   }
 #pragma unroll
