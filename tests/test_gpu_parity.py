@@ -552,3 +552,48 @@ def test_alternating_wavefront_equals_serial(name, nwin, monkeypatch):
     assert np.array_equal(a.psi, b.psi)
     assert np.array_equal(a.mesh.coords, b.mesh.coords)
     assert all(np.array_equal(x, y) for x, y in zip(a.sub_psi, b.sub_psi))
+
+
+@pytest.mark.parametrize("case", ["huge_det", "tiny_det", "deep_saturation", "nan_node"])
+def test_rkc_step_extreme_values(case):
+    """The window kernel's two-node log-equidistribution (logequi_pair) takes
+    a straight-line path when every operand is in range and logequi() itself
+    otherwise: determinants beyond the 1e+-290 range of the reciprocal-multiply
+    quotient, a saturation denominator beyond 2^100, a NaN.  One RKC2 step on a
+    C1 box with such nodes planted, against the oracle (integrate.py:163-178,
+    pma.py:186-192): same flags, same values (NaN where the oracle has NaN)."""
+    g, d, mon = ring_case()
+    og = O.make_grid(2, ((0, 1), (0, 1)), (65, 65))
+    od = O.make_decomposition(og, (2, 2), 4)
+    geom = P.subdomain_geometry(g, d.subdomains[0])
+    ogeom = O.box_geom(og, od.subs[0])
+    y = R.perturbed_global(geom.axes).copy()
+    if case == "huge_det":          # |det| ~ 1e300: outside the Markstein range, true division
+        y[12, 12] += 3e146
+        y[20, 21] -= 2e147
+    elif case == "tiny_det":        # det ~ 1e-300-scale products are not reachable; tiny positive det
+        y[:] = 0.5 * (geom.axes[0][:, None] ** 2 + geom.axes[1][None, :] ** 2) * 1e-160
+    elif case == "deep_saturation":  # det / guard ~ -1e40: saturation denominator > 2^100
+        y[15, 15] += 1e18
+        y[15, 16] -= 1e18
+    else:
+        y[9, 11] = np.nan
+    coords = np.stack(O.coords_fd(np.nan_to_num(R.perturbed_global(geom.axes)), ogeom), axis=-1)
+    rho = O.Ring()(np.clip(coords, 0, 1)) / 1.3
+    rmax = float(rho.max())
+    with np.errstate(all="ignore"):
+        fn = lambda v: O.rhs_frozen(v, rho, ogeom, O.DET_FLOOR, ogeom.mask(), rmax)
+        f0, _ = fn(y)
+        od_, ofn, ofl, oend = O.Rkc2(1e-3)._step(y, f0, 1e-7, 3, fn)
+    with Plan.for_geometry(geom, P.SolverConfig()) as p:
+        dd, fnew, fl, end = p.rkc_step(0, y, rho, rmax, 1e-7, 3)
+    assert (fl, end) == (ofl, oend), case
+    for got, ref, name in ((dd, od_, "d"), (fnew, ofn, "f")):
+        assert np.array_equal(np.isnan(got), np.isnan(ref)), (case, name)
+        assert np.array_equal(np.isinf(got), np.isinf(ref)), (case, name)
+        fin = np.isfinite(ref)
+        assert np.array_equal(np.sign(got[~fin & ~np.isnan(ref)]), np.sign(ref[~fin & ~np.isnan(ref)]))
+        scale = max(float(np.max(np.abs(ref[fin]))), 1e-300)
+        err = float(np.max(np.abs(got[fin] - ref[fin]))) / scale
+        print(f"[parity] rkc_step extreme {case} {name}: rel err {err:.3g}")
+        assert err <= 1e-12, (case, name, err)
