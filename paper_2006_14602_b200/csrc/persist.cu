@@ -1205,7 +1205,11 @@ __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, cons
   const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
   const int i1 = r0 + threadIdx.y, i2 = c0 + threadIdx.x;
   const long long plane = (long long)n1 * g.pitch;
+  static_assert(IZ3 == 2, "logequi_pair handles the two nodes of a thread");
   double ps = 0.0;
+  double detq[IZ3] = {1.0, 1.0}, Fq[IZ3] = {0.0, 0.0};
+  unsigned validm = 0u, dirm = 0u;   // bit q: node q inside the box / on an interface face
+  // phase 1: determinants of both nodes
 #pragma unroll
   for (int q = 0; q < IZ3; ++q) {
     const int i0 = z0 + q;
@@ -1256,11 +1260,34 @@ __device__ __forceinline__ void compute3(const WinArgs& A, const SubGeo& g, cons
       // box-face nodes: interface (Dirichlet) faces need no determinant (F = 0,
       // never flagged); physical faces take the Neumann-ghost formulas
       const bool dir = !interior && dirichlet<3>(g, i0, i1, i2);
+      // box-face nodes: interface (Dirichlet) faces need no determinant (F = 0,
+      // never flagged); physical faces take the Neumann-ghost formulas
       if (!interior)
         det = dir ? 0.0
                   : hdet3_face<P2, YM>(A.P, g, i0, i1, i2, st, p, t.c, (i0 + i1 + i2) & 1);
-      const double F = dir ? 0.0 : logequi(st.cm[pc], det, A.P.guard, A.P.floor, A.P.rguard, s_logtab);
-      acc.flag |= (det <= A.P.floor && !dir) ? 1u : 0u;
+      detq[q] = det;
+      validm |= 1u << q;
+      dirm |= dir ? (1u << q) : 0u;
+    }
+  }
+  if constexpr (MODE != M_NORM) {
+    // phase 2: log-equidistribution of both nodes, interleaved (logequi_pair)
+    const double mrv[2] = {st.cm[threadIdx.y * TX + threadIdx.x],
+                           st.cm[(TY + threadIdx.y) * TX + threadIdx.x]};
+    const double g_ = A.P.guard;
+    logequi_pair(mrv, detq, dirm | (~validm & 3u), g_, A.P.floor, A.P.rguard,
+                 g_ >= 0x1p-900 && g_ < 0x1p900, s_logtab, Fq);
+    // phase 3: epilogues
+#pragma unroll
+    for (int q = 0; q < IZ3; ++q) {
+      if (!((validm >> q) & 1u)) continue;
+      const int i0 = z0 + q;
+      const int p = ((q + 1) * TH3 + threadIdx.y + 1) * TW2 + threadIdx.x + 2;
+      const int pc = (q * TY + threadIdx.y) * TX + threadIdx.x;
+      const long long k = g.off + i0 * plane + (long long)i1 * g.pitch + i2;
+      const bool dir = (dirm >> q) & 1u;
+      const double F = Fq[q];
+      acc.flag |= (detq[q] <= A.P.floor && !dir) ? 1u : 0u;
       if constexpr (MODE == M_F0) {
         A.F.f[t.fi][k] = F;
       } else if constexpr (MODE == M_EULER) {
